@@ -1,0 +1,142 @@
+/*
+ * idw_b200.h -- C ABI of libidw_b200.so, the sm_100a all-pairs IDW engine.
+ *
+ * The reference (`idwlayout`, pure Python + numba) has no FFI: its hot path is
+ * an in-process call from the strategy layer into numba-compiled loops.  This
+ * header is the seam that replaces those calls.  Every entry point names the
+ * reference code it stands in for (paths relative to /root/reference/pkg/src).
+ *
+ *   idw_run / idw_run_device   replace the strategy bodies that drive
+ *                              kernels.predict_block        (kernels.py:34-67,
+ *                                 via strategies.run_naive   strategies.py:148-166
+ *                                 and core.idw_predict_seq   core.py:119-148)
+ *                              kernels.tile_accumulate +
+ *                              kernels.finalize_block      (kernels.py:70-108,
+ *                                 via strategies.run_tiled   strategies.py:169-199)
+ *                              kernels.nested_improved_block +
+ *                              kernels._tree_combine       (kernels.py:111-185,
+ *                                 via strategies.run_nested_improved :234-261)
+ *                              kernels.nested_original_block (kernels.py:188-248,
+ *                                 via strategies.run_nested_original :202-231)
+ *
+ * Conventions
+ *   - Plain C types only; no torch or CUDA types in signatures.
+ *   - Every function returns 0 on success or a negative IDW_E* code; the
+ *     message of the last failure on the calling thread is idw_last_error().
+ *   - Validation that the reference performs in Python (core.py:93-116,
+ *     layouts.py:80-82, strategies.py:125-134) stays in the Python host layer;
+ *     the library re-checks structural arguments and fails loudly.
+ *   - There is no CPU fallback: without a usable CUDA device every compute
+ *     entry point returns IDW_E_CUDA.
+ */
+#ifndef IDW_B200_H
+#define IDW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IDW_ABI_VERSION 1
+
+/* Layout kind codes == layouts._KIND_CODES (enum order, layouts.py:43-65). */
+enum idw_kind { IDW_SOA = 0, IDW_AOS = 1, IDW_AOAS = 2, IDW_SOAOS = 3, IDW_HYBRID = 4 };
+
+/* Precision codes == layouts._PRECISION_CODES (layouts.py:66). */
+enum idw_precision { IDW_SINGLE = 0, IDW_DOUBLE = 1 };
+
+/* Strategy codes, in strategies.STRATEGIES order (strategies.py:264-269). */
+enum idw_variant {
+  IDW_NAIVE = 0,            /* K1: one query per thread, global broadcast loads   */
+  IDW_TILED = 1,            /* K2: smem tiles staged by cp.async.bulk + mbarriers */
+  IDW_NESTED_ORIGINAL = 2,  /* K4: per-group tree + serial merge (paper "original CDP") */
+  IDW_NESTED_IMPROVED = 3   /* K3: G strided lanes + xor-shuffle adjacent-pair tree */
+};
+
+/* Arithmetic mode.
+ *   EXACT: IEEE round-to-nearest ops in the reference's order; p = 2 results are
+ *          bit-identical to the numba reference (no FMA contraction, correctly
+ *          rounded 1/d2).  General p uses CUDA pow (few-ulp from glibc pow).
+ *   FAST:  MUFU rcp.approx (p = 2) / ex2(lg2 * wexp) (general p), FMA contraction,
+ *          packed f32x2 arithmetic, per-tile (tiled) or per-chunk (nested)
+ *          partial sums folded with compensated addition.  Coincident queries
+ *          are detected and recomputed exactly by a fix-up pass.           */
+enum idw_mode { IDW_EXACT = 0, IDW_FAST = 1 };
+
+enum idw_err {
+  IDW_OK = 0,
+  IDW_E_ARG = -1,         /* malformed argument (kind/precision/buffers/sizes)  */
+  IDW_E_UNSUPPORTED = -2, /* illegal layout/precision pair or variant         */
+  IDW_E_CUDA = -3,        /* CUDA runtime failure or no device                */
+  IDW_E_NOMEM = -4        /* device allocation failure                        */
+};
+
+/* A point store == layouts.LayoutStore (layouts.py:143-170): kind, precision,
+ * count and its raw byte buffers in buffer_shapes() order (layouts.py:85-104).
+ * Buffers hold the exact bytes the reference packs (strides 4/8, 12/24,
+ * 16/32, 16+16, 16+8); pads are never read as data.                        */
+typedef struct idw_store {
+  int32_t kind;            /* enum idw_kind                                   */
+  int32_t precision;       /* enum idw_precision                              */
+  int64_t count;           /* n >= 1                                          */
+  int32_t nbuf;            /* number of buffers for `kind` (3, 1, 1, 2, 2)     */
+  int32_t reserved;
+  const void *buf[3];      /* buffer base pointers (host or device, see call) */
+  int64_t nbytes[3];       /* == BufferSpec.nbytes                            */
+} idw_store;
+
+/* Params (core.py:31-47) + ExecConfig (strategies.py:41-66) + GPU knobs. */
+typedef struct idw_params {
+  double p;                /* power, > 0; p == 2 takes the reciprocal path    */
+  double zero_eps;         /* coincidence threshold on d2, >= 0               */
+  int32_t variant;         /* enum idw_variant                                */
+  int32_t mode;            /* enum idw_mode                                   */
+  int64_t group_size;      /* G (nested lanes per query; tiled query group)   */
+  int64_t tile_size;       /* T (reference staging tile; informational)       */
+  int32_t splits;          /* FAST tiled: data splits (0 = auto, 1 = none)    */
+  int32_t device;          /* CUDA device ordinal for this call               */
+} idw_params;
+
+/* Optional per-call instrumentation (RunStats, strategies.py:104-115). */
+typedef struct idw_stats {
+  int64_t merge_events;    /* nested_original: m * ceil(n/G); others 0        */
+  int64_t kernel_launches; /* kernels this call launched                      */
+  double kernel_ms;        /* device time of the compute kernels (events)     */
+  int64_t fixup_queries;   /* FAST: queries recomputed exactly (coincidence)  */
+} idw_stats;
+
+/* ABI version (IDW_ABI_VERSION) -- lets the ctypes loader refuse stale builds. */
+int idw_abi_version(void);
+
+/* Number of visible CUDA devices (0 if none); never fails. */
+int idw_device_count(void);
+
+/* Message of the last error on this thread ("" if none). */
+const char *idw_last_error(void);
+
+/* Blocking run over HOST memory: copies the store buffers and the query
+ * coordinates (qx, qy: m values of the run dtype each, already cast RN as in
+ * strategies._prepare, strategies.py:125-134) to the device, runs the variant,
+ * and writes m run-dtype predictions into `out`.  `stats` may be NULL.
+ * Replaces one whole strategies.run_* call body.                          */
+int idw_run(const idw_store *store, const void *qx, const void *qy, int64_t m,
+            const idw_params *prm, void *out, idw_stats *stats);
+
+/* Asynchronous run over DEVICE memory on `stream` (a cudaStream_t, NULL =
+ * legacy default stream).  Store buffers must stay readable up to
+ * nbytes rounded up to 16 bytes (bulk copies move 16-byte granules).  Scratch
+ * is stream-ordered (cudaMallocAsync).  stats->kernel_ms is not filled here. */
+int idw_run_device(const idw_store *store, const void *qx, const void *qy, int64_t m,
+                   const idw_params *prm, void *out, void *stream, idw_stats *stats);
+
+/* Measured MUFU reciprocal rate of `device`: a register-resident loop of
+ * independent rcp.approx.f32 over all SMs, timed with events.  Writes
+ * rcp results per second (== the p = 2 fp32 pair roofline) and the mean SM
+ * clock implied by the kernel's clock64() cycle count.                   */
+int idw_mufu_peak(int device, double *rcp_per_s, double *sm_hz);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IDW_B200_H */

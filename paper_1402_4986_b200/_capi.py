@@ -1,0 +1,177 @@
+"""ctypes binding of ``libidw_b200.so`` (declared in ``include/idw_b200.h``).
+
+This is the only module that touches the native library.  It loads the
+in-tree build (``paper_1402_4986_b200/libidw_b200.so``) and raises loudly when
+it is missing or stale: the package has no CPU fallback, by design.  ctypes
+releases the GIL for the duration of every call, like the reference's
+``@njit(nogil=True)`` kernels (reference kernels.py:34).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+ABI_VERSION = 1
+
+# enum codes -- include/idw_b200.h
+KIND_CODES = {"soa": 0, "aos": 1, "aoas": 2, "soaos": 3, "hybrid": 4}  # layouts.py:65
+PRECISION_CODES = {"single": 0, "double": 1}                            # layouts.py:66
+VARIANT_CODES = {"naive": 0, "tiled": 1, "nested_original": 2, "nested_improved": 3}
+MODE_CODES = {"exact": 0, "fast": 1}
+
+_LIB_NAME = "libidw_b200.so"
+
+
+class IdwStore(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("precision", ctypes.c_int32),
+        ("count", ctypes.c_int64),
+        ("nbuf", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("buf", ctypes.c_void_p * 3),
+        ("nbytes", ctypes.c_int64 * 3),
+    ]
+
+
+class IdwParams(ctypes.Structure):
+    _fields_ = [
+        ("p", ctypes.c_double),
+        ("zero_eps", ctypes.c_double),
+        ("variant", ctypes.c_int32),
+        ("mode", ctypes.c_int32),
+        ("group_size", ctypes.c_int64),
+        ("tile_size", ctypes.c_int64),
+        ("splits", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+    ]
+
+
+class IdwStats(ctypes.Structure):
+    _fields_ = [
+        ("merge_events", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64),
+        ("kernel_ms", ctypes.c_double),
+        ("fixup_queries", ctypes.c_int64),
+    ]
+
+
+EXPORTS = ("idw_abi_version", "idw_device_count", "idw_last_error", "idw_run",
+           "idw_run_device", "idw_mufu_peak")
+
+
+class NativeError(RuntimeError):
+    """A libidw_b200 call failed; the message is ``idw_last_error()``."""
+
+
+def library_path() -> Path:
+    override = os.environ.get("IDW_B200_LIB")
+    if override:
+        return Path(override)
+    return Path(__file__).resolve().parent / _LIB_NAME
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load (once) and type the native library; raise if absent or stale."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = library_path()
+    if not path.exists():
+        raise ImportError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            f"or `make -C paper_1402_4986_b200/csrc` (there is no CPU fallback)")
+    lib = ctypes.CDLL(str(path))
+    lib.idw_abi_version.restype = ctypes.c_int
+    lib.idw_abi_version.argtypes = []
+    if lib.idw_abi_version() != ABI_VERSION:
+        raise ImportError(f"{path}: ABI {lib.idw_abi_version()} != expected {ABI_VERSION}; rebuild")
+    lib.idw_device_count.restype = ctypes.c_int
+    lib.idw_device_count.argtypes = []
+    lib.idw_last_error.restype = ctypes.c_char_p
+    lib.idw_last_error.argtypes = []
+    ptr = ctypes.c_void_p
+    lib.idw_run.restype = ctypes.c_int
+    lib.idw_run.argtypes = [ctypes.POINTER(IdwStore), ptr, ptr, ctypes.c_int64,
+                            ctypes.POINTER(IdwParams), ptr, ctypes.POINTER(IdwStats)]
+    lib.idw_run_device.restype = ctypes.c_int
+    lib.idw_run_device.argtypes = [ctypes.POINTER(IdwStore), ptr, ptr, ctypes.c_int64,
+                                   ctypes.POINTER(IdwParams), ptr, ptr, ctypes.POINTER(IdwStats)]
+    lib.idw_mufu_peak.restype = ctypes.c_int
+    lib.idw_mufu_peak.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_double)]
+    _lib = lib
+    return lib
+
+
+def device_count() -> int:
+    return int(load().idw_device_count())
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = load().idw_last_error().decode("utf-8", "replace")
+        raise NativeError(f"libidw_b200 error {rc}: {msg}")
+
+
+def make_store(kind: str, precision: str, count: int, pointers, nbytes) -> IdwStore:
+    s = IdwStore()
+    s.kind = KIND_CODES[kind]
+    s.precision = PRECISION_CODES[precision]
+    s.count = int(count)
+    s.nbuf = len(pointers)
+    for i, (p, nb) in enumerate(zip(pointers, nbytes)):
+        s.buf[i] = int(p)
+        s.nbytes[i] = int(nb)
+    return s
+
+
+def make_params(p: float, zero_eps: float, variant: str, mode: str, group_size: int,
+                tile_size: int, splits: int = 0, device: int = 0) -> IdwParams:
+    prm = IdwParams()
+    prm.p = float(p)
+    prm.zero_eps = float(zero_eps)
+    prm.variant = VARIANT_CODES[variant]
+    prm.mode = MODE_CODES[mode]
+    prm.group_size = int(group_size)
+    prm.tile_size = int(tile_size)
+    prm.splits = int(splits)
+    prm.device = int(device)
+    return prm
+
+
+def run_host(store: IdwStore, qx: np.ndarray, qy: np.ndarray, params: IdwParams,
+             out: np.ndarray) -> IdwStats:
+    """Blocking ``idw_run`` over host arrays (qx, qy, out contiguous, run dtype)."""
+    lib = load()
+    stats = IdwStats()
+    m = out.shape[0]
+    _check(lib.idw_run(ctypes.byref(store), qx.ctypes.data, qy.ctypes.data, m,
+                       ctypes.byref(params), out.ctypes.data, ctypes.byref(stats)))
+    return stats
+
+
+def run_device(store: IdwStore, qx_ptr: int, qy_ptr: int, m: int, params: IdwParams,
+               out_ptr: int, stream: int = 0) -> IdwStats:
+    """Asynchronous ``idw_run_device`` over device pointers on ``stream``."""
+    lib = load()
+    stats = IdwStats()
+    _check(lib.idw_run_device(ctypes.byref(store), qx_ptr, qy_ptr, m, ctypes.byref(params),
+                              out_ptr, stream, ctypes.byref(stats)))
+    return stats
+
+
+def mufu_peak(device: int = 0) -> tuple[float, float]:
+    """(rcp results per second, implied SM clock in Hz) measured on ``device``."""
+    lib = load()
+    rate = ctypes.c_double()
+    hz = ctypes.c_double()
+    _check(lib.idw_mufu_peak(device, ctypes.byref(rate), ctypes.byref(hz)))
+    return rate.value, hz.value

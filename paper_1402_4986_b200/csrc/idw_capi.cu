@@ -1,0 +1,298 @@
+// idw_capi.cu -- the extern "C" shim of libidw_b200.so (include/idw_b200.h).
+//
+// One call == one reference strategy call (strategies.py:148-261): validate the
+// structural arguments, stage host buffers into HBM when the caller passed host
+// memory, launch the variant kernel (+ the exact fix-up pass in FAST mode) on a
+// per-device stream, and copy the predictions back.  No CPU fallback exists.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "idw_launch.h"
+
+namespace idw {
+
+// ===========================================================================
+// MUFU roofline probe: independent rcp.approx chains, 8 per thread.
+static __global__ void k_mufu_probe(float *out, int iters, unsigned long long *cycles) {
+  float a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1.0f + 1e-3f * (threadIdx.x + k);
+  long long c0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(a[k]));
+  }
+  long long c1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) cycles[0] = (unsigned long long)(c1 - c0);
+}
+
+
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+
+static int bytes_per_point(int kind, int prec, int b) {
+  const int e = prec == IDW_SINGLE ? 4 : 8;
+  switch (kind) {
+    case IDW_SOA: return e;
+    case IDW_AOS: return 3 * e;
+    case IDW_AOAS: return 4 * e;
+    case IDW_SOAOS: return 16;
+    case IDW_HYBRID: return b == 0 ? 16 : 8;
+  }
+  return 0;
+}
+static int nbuf_of(int kind) {
+  return kind == IDW_SOA ? 3 : (kind == IDW_AOS || kind == IDW_AOAS) ? 1 : 2;
+}
+
+static int validate(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p,
+                    const void *out) {
+  if (!s || !p) return set_error("null store or params"), IDW_E_ARG;
+  if (s->kind < 0 || s->kind > 4) return set_error("unknown layout kind"), IDW_E_ARG;
+  if (s->precision != IDW_SINGLE && s->precision != IDW_DOUBLE) return set_error("unknown precision"), IDW_E_ARG;
+  if (s->precision == IDW_SINGLE && (s->kind == IDW_SOAOS || s->kind == IDW_HYBRID))
+    return set_error("layout requires double precision"), IDW_E_UNSUPPORTED;  // layouts.py:80-82
+  if (s->count < 1) return set_error("no data points"), IDW_E_ARG;           // strategies.py:128-129
+  if (s->nbuf != nbuf_of(s->kind)) return set_error("buffer count does not match layout"), IDW_E_ARG;
+  for (int b = 0; b < s->nbuf; ++b) {
+    if (!s->buf[b]) return set_error("null store buffer"), IDW_E_ARG;
+    const int64_t need = s->count * (int64_t)bytes_per_point(s->kind, s->precision, b);
+    if (s->nbytes[b] < need) return set_error("store buffer shorter than its shape"), IDW_E_ARG;
+    const int align = s->kind == IDW_AOS ? (s->precision == IDW_SINGLE ? 4 : 8) : 16;
+    if (((uintptr_t)s->buf[b]) % 16 != 0 && align == 16)
+      return set_error("store buffer not 16-byte aligned"), IDW_E_ARG;
+  }
+  if (m < 0) return set_error("negative query count"), IDW_E_ARG;
+  if (m > 0 && (!qx || !qy || !out)) return set_error("null query or output pointer"), IDW_E_ARG;
+  if (!(p->p > 0)) return set_error("power p must be > 0"), IDW_E_ARG;          // core.py:43-44
+  if (!(p->zero_eps >= 0)) return set_error("zero_eps must be >= 0"), IDW_E_ARG;  // core.py:45-46
+  if (p->variant < IDW_NAIVE || p->variant > IDW_NESTED_IMPROVED) return set_error("unknown variant"), IDW_E_ARG;
+  if (p->mode != IDW_EXACT && p->mode != IDW_FAST) return set_error("unknown mode"), IDW_E_ARG;
+  if (p->group_size < 1) return set_error("group_size must be >= 1"), IDW_E_ARG;  // strategies.py:57-58
+  if (p->tile_size < 1) return set_error("tile_size must be >= 1"), IDW_E_ARG;
+  if (p->splits < 0) return set_error("splits must be >= 0"), IDW_E_ARG;
+  return 0;
+}
+
+static std::mutex g_mu;
+static cudaStream_t g_streams[64];
+static int g_sms[64];
+
+static int device_stream(int dev, cudaStream_t *st, int *sms) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    set_error("no CUDA device available (libidw_b200 has no CPU fallback)");
+    return IDW_E_CUDA;
+  }
+  if (dev < 0 || dev >= ndev || dev >= 64) return set_error("device ordinal out of range"), IDW_E_ARG;
+  IDW_CK(cudaSetDevice(dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_streams[dev]) {
+    IDW_CK(cudaStreamCreateWithFlags(&g_streams[dev], cudaStreamNonBlocking));
+    IDW_CK(cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev));
+  }
+  *st = g_streams[dev];
+  *sms = g_sms[dev];
+  return 0;
+}
+
+static void fill_launch(Launch &L, const idw_store *s, const void *const *bufs, const void *qx, const void *qy,
+                        int64_t m, const idw_params *p, void *out) {
+  L.kind = s->kind;
+  L.prec = s->precision;
+  L.mode = p->mode;
+  L.variant = p->variant;
+  L.p2 = (p->p == 2.0);  // kernels.scalar_args: fast = p == 2.0 (kernels.py:22)
+  L.epsp = p->zero_eps > 0;
+  for (int b = 0; b < 3; ++b) L.g.b[b] = (const unsigned char *)(b < s->nbuf ? bufs[b] : nullptr);
+  L.n = s->count;
+  L.qx = qx;
+  L.qy = qy;
+  L.m = m;
+  L.eps = p->zero_eps;
+  L.wexp = -p->p / 2.0;
+  // FAST screen: inflate eps by 2^-16 relative so FMA-contracted d2 can never
+  // hide an exact coincidence; the fix-up re-tests with IEEE d2.
+  L.eps_flag = p->zero_eps * (1.0 + 1.0 / 65536.0);
+  L.G = p->group_size;
+  L.T = p->tile_size;
+  L.splits = p->splits;
+  L.out = out;
+}
+
+static int dispatch(Launch &L) {
+  int rc = 0;
+  switch (L.variant) {
+    case IDW_NAIVE: rc = launch_naive(L); break;
+    case IDW_TILED: rc = launch_tiled(L); break;
+    case IDW_NESTED_IMPROVED: rc = launch_nested(L); break;
+    case IDW_NESTED_ORIGINAL: rc = launch_nested_orig(L); break;
+    default: set_error("unknown variant"); return IDW_E_ARG;
+  }
+  if (rc) return rc;
+  if (L.mode == IDW_FAST && L.variant != IDW_NESTED_ORIGINAL) rc = launch_fixup(L);
+  return rc;
+}
+
+static void fill_stats(idw_stats *st, const Launch &L, const idw_params *p, int64_t n, int64_t m) {
+  if (!st) return;
+  st->kernel_launches = L.launches;
+  st->merge_events = p->variant == IDW_NESTED_ORIGINAL ? m * ((n + p->group_size - 1) / p->group_size) : 0;
+}
+
+}  // namespace idw
+
+using namespace idw;
+
+extern "C" {
+
+int idw_abi_version(void) { return IDW_ABI_VERSION; }
+
+int idw_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+const char *idw_last_error(void) { return g_err.c_str(); }
+
+int idw_run_device(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p, void *out,
+                   void *stream, idw_stats *stats) {
+  g_err.clear();
+  int rc = validate(s, qx, qy, m, p, out);
+  if (rc) return rc;
+  if (m == 0) return 0;
+  cudaStream_t dst;
+  int sms;
+  if ((rc = device_stream(p->device, &dst, &sms))) return rc;
+  Launch L;
+  fill_launch(L, s, s->buf, qx, qy, m, p, out);
+  L.st = (cudaStream_t)stream;
+  L.dev = p->device;
+  L.sms = sms;
+  unsigned char *flags = nullptr;
+  if (p->mode == IDW_FAST) {
+    IDW_CK(cudaMallocAsync((void **)&flags, (size_t)m, L.st));
+    L.flags = flags;
+  }
+  rc = dispatch(L);
+  if (flags) cudaFreeAsync(flags, L.st);
+  fill_stats(stats, L, p, s->count, m);
+  return rc;
+}
+
+int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p, void *out,
+            idw_stats *stats) {
+  g_err.clear();
+  int rc = validate(s, qx, qy, m, p, out);
+  if (rc) return rc;
+  if (m == 0) return 0;
+  cudaStream_t st;
+  int sms;
+  if ((rc = device_stream(p->device, &st, &sms))) return rc;
+  const size_t esz = s->precision == IDW_SINGLE ? 4 : 8;
+  // one stream-ordered arena: buffers (padded to 16 B + 64 B slack for the
+  // rounded-up bulk copy of the tail tile), qx, qy, out, flags, fix-up counter
+  size_t off[8], total = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = total;
+    total += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  for (int b = 0; b < s->nbuf; ++b) off[b] = take((size_t)s->nbytes[b] + 64);
+  off[3] = take(esz * (size_t)m);
+  off[4] = take(esz * (size_t)m);
+  off[5] = take(esz * (size_t)m);
+  off[6] = take((size_t)m);
+  off[7] = take(sizeof(unsigned long long));
+  unsigned char *arena = nullptr;
+  IDW_CK(cudaMallocAsync((void **)&arena, total, st));
+  const void *dbuf[3] = {nullptr, nullptr, nullptr};
+  for (int b = 0; b < s->nbuf; ++b) {
+    IDW_CK(cudaMemcpyAsync(arena + off[b], s->buf[b], (size_t)s->nbytes[b], cudaMemcpyHostToDevice, st));
+    dbuf[b] = arena + off[b];
+  }
+  IDW_CK(cudaMemcpyAsync(arena + off[3], qx, esz * (size_t)m, cudaMemcpyHostToDevice, st));
+  IDW_CK(cudaMemcpyAsync(arena + off[4], qy, esz * (size_t)m, cudaMemcpyHostToDevice, st));
+  IDW_CK(cudaMemsetAsync(arena + off[7], 0, sizeof(unsigned long long), st));
+  Launch L;
+  fill_launch(L, s, dbuf, arena + off[3], arena + off[4], m, p, arena + off[5]);
+  L.st = st;
+  L.dev = p->device;
+  L.sms = sms;
+  if (p->mode == IDW_FAST) L.flags = arena + off[6];
+  L.nfixed = (unsigned long long *)(arena + off[7]);
+  cudaEvent_t e0, e1;
+  IDW_CK(cudaEventCreate(&e0));
+  IDW_CK(cudaEventCreate(&e1));
+  IDW_CK(cudaEventRecord(e0, st));
+  rc = dispatch(L);
+  if (rc == 0) {
+    IDW_CK(cudaEventRecord(e1, st));
+    IDW_CK(cudaMemcpyAsync(out, arena + off[5], esz * (size_t)m, cudaMemcpyDeviceToHost, st));
+    unsigned long long nfix = 0;
+    IDW_CK(cudaMemcpyAsync(&nfix, L.nfixed, sizeof(nfix), cudaMemcpyDeviceToHost, st));
+    IDW_CK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (stats) {
+      stats->kernel_ms = ms;
+      stats->fixup_queries = (int64_t)nfix;
+    }
+  }
+  cudaFreeAsync(arena, st);
+  cudaStreamSynchronize(st);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  fill_stats(stats, L, p, s->count, m);
+  return rc;
+}
+
+int idw_mufu_peak(int device, double *rcp_per_s, double *sm_hz) {
+  g_err.clear();
+  cudaStream_t st;
+  int sms, rc;
+  if ((rc = device_stream(device, &st, &sms))) return rc;
+  float *dout = nullptr;
+  unsigned long long *dcyc = nullptr;
+  IDW_CK(cudaMallocAsync((void **)&dout, 16, st));
+  IDW_CK(cudaMallocAsync((void **)&dcyc, 16, st));
+  const int blocks = sms * 8, threads = 256, iters = 8192;
+  cudaEvent_t e0, e1;
+  IDW_CK(cudaEventCreate(&e0));
+  IDW_CK(cudaEventCreate(&e1));
+  k_mufu_probe<<<blocks, threads, 0, st>>>(dout, 256, dcyc);  // warm-up
+  IDW_CK_LAUNCH();
+  IDW_CK(cudaEventRecord(e0, st));
+  k_mufu_probe<<<blocks, threads, 0, st>>>(dout, iters, dcyc);
+  IDW_CK_LAUNCH();
+  IDW_CK(cudaEventRecord(e1, st));
+  unsigned long long cyc = 0;
+  IDW_CK(cudaMemcpyAsync(&cyc, dcyc, sizeof(cyc), cudaMemcpyDeviceToHost, st));
+  IDW_CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  IDW_CK(cudaEventElapsedTime(&ms, e0, e1));
+  const double ops = (double)blocks * threads * 8.0 * iters;
+  if (rcp_per_s) *rcp_per_s = ops / (ms * 1e-3);
+  if (sm_hz) *sm_hz = (double)cyc / (ms * 1e-3);
+  cudaFreeAsync(dout, st);
+  cudaFreeAsync(dcyc, st);
+  cudaStreamSynchronize(st);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return 0;
+}
+
+}  // extern "C"

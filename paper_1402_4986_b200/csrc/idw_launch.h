@@ -1,0 +1,105 @@
+// idw_launch.h -- host-side launch plumbing shared by the per-variant
+// translation units (compiled in parallel) and the C-ABI shim.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <type_traits>
+
+#include "../../include/idw_b200.h"
+#include "idw_common.cuh"
+
+namespace idw {
+
+// Everything a variant launcher needs; all pointers are device pointers.
+struct Launch {
+  int kind = 0, prec = 0, mode = 0, variant = 0;
+  bool p2 = true, epsp = false;
+  Bufs g{};
+  long long n = 0;
+  const void *qx = nullptr, *qy = nullptr;
+  long long m = 0;
+  double eps = 0.0, wexp = -1.0, eps_flag = 0.0;
+  long long G = 1024, T = 1024;
+  int splits = 0;
+  void *out = nullptr;
+  unsigned char *flags = nullptr;  // FAST: m bytes of screen flags
+  unsigned long long *nfixed = nullptr;
+  cudaStream_t st = nullptr;
+  int dev = 0, sms = 148;
+  int launches = 0;
+};
+
+void set_error(const std::string &msg);
+
+#define IDW_CK(call)                                                                    \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      ::idw::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));             \
+      return (int)IDW_E_CUDA;                                                           \
+    }                                                                                   \
+  } while (0)
+
+#define IDW_CK_LAUNCH()                                                                 \
+  do {                                                                                  \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess) {                                                            \
+      ::idw::set_error(std::string("kernel launch: ") + cudaGetErrorString(e_));        \
+      return (int)IDW_E_CUDA;                                                           \
+    }                                                                                   \
+  } while (0)
+
+template <int V>
+using IC = std::integral_constant<int, V>;
+template <bool V>
+using BC = std::integral_constant<bool, V>;
+
+// Visit the legal (layout, dtype) pair of a launch (layouts.legal_pairs,
+// layouts.py:317-319): SoAoS and Hybrid exist only in double precision.
+template <class F>
+int with_layout(const Launch &L, F &&f) {
+  if (L.prec == IDW_SINGLE) {
+    switch (L.kind) {
+      case SOA: return f(IC<SOA>{}, float{});
+      case AOS: return f(IC<AOS>{}, float{});
+      case AOAS: return f(IC<AOAS>{}, float{});
+      default: set_error("layout requires double precision"); return IDW_E_UNSUPPORTED;
+    }
+  }
+  switch (L.kind) {
+    case SOA: return f(IC<SOA>{}, double{});
+    case AOS: return f(IC<AOS>{}, double{});
+    case AOAS: return f(IC<AOAS>{}, double{});
+    case SOAOS: return f(IC<SOAOS>{}, double{});
+    case HYBRID: return f(IC<HYBRID>{}, double{});
+    default: set_error("unknown layout kind"); return IDW_E_ARG;
+  }
+}
+
+// Visit (mode, p == 2, zero_eps > 0).  EXACT always tests coincidence in the
+// loop, so only FAST distinguishes the eps flag.
+template <class F>
+int with_arith(const Launch &L, F &&f) {
+  if (L.mode == EXACT) return L.p2 ? f(IC<EXACT>{}, BC<true>{}, BC<false>{}) : f(IC<EXACT>{}, BC<false>{}, BC<false>{});
+  if (L.p2) return L.epsp ? f(IC<FAST>{}, BC<true>{}, BC<true>{}) : f(IC<FAST>{}, BC<true>{}, BC<false>{});
+  return L.epsp ? f(IC<FAST>{}, BC<false>{}, BC<true>{}) : f(IC<FAST>{}, BC<false>{}, BC<false>{});
+}
+
+template <typename T>
+inline Scal<T> make_scal(const Launch &L) {
+  Scal<T> s;
+  s.eps = (T)L.eps;
+  s.wexp = (T)L.wexp;
+  s.eps_flag = (T)L.eps_flag;
+  return s;
+}
+
+// Per-variant launchers (one translation unit each).
+int launch_naive(Launch &L);
+int launch_tiled(Launch &L);
+int launch_nested(Launch &L);
+int launch_nested_orig(Launch &L);
+int launch_fixup(Launch &L);
+
+}  // namespace idw

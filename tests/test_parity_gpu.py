@@ -1,0 +1,153 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's bits.
+
+EXACT mode must reproduce the reference bit-for-bit for p = 2 (every layout,
+precision, strategy, G and T of the golden matrix).  General p goes through
+CUDA pow instead of glibc pow, so it is held to the north-star tolerances
+(1e-5 single, 1e-12 double).  FAST mode is held to those tolerances against
+the fp64 double-double truth of the oracle, with coincident queries exact.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden_case, random_queries, random_records
+
+pytestmark = pytest.mark.gpu
+
+STRATS = ("naive", "tiled", "nested_original", "nested_improved")
+TOL = {"single": 1e-5, "double": 1e-12}
+
+
+@pytest.fixture(scope="module")
+def il():
+    import paper_1402_4986_b200 as pkg
+
+    if pkg._capi.device_count() < 1:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+    return pkg
+
+
+def _names(g):
+    return [str(s) for s in g["names"]]
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))) if a.size else 0.0
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_exact_mode_matches_reference_golden(il, golden, strategy):
+    for name in _names(golden):
+        data, queries, p, eps, G, T = golden_case(golden, name)
+        cfg = il.ExecConfig(group_size=G, tile_size=T, mode="exact")
+        for kind, precision in il.legal_pairs():
+            store = il.build(data, kind, precision)
+            got = il.STRATEGIES[strategy](store, queries, il.Params(p, eps), cfg)
+            ref = golden[f"{name}/{precision.value}/{kind.value}/{strategy}"]
+            assert got.dtype == ref.dtype
+            if p == 2.0:
+                assert np.array_equal(got.view(np.uint8), ref.view(np.uint8)), (name, kind, precision, strategy)
+            else:
+                assert rel(got, ref) <= TOL[precision.value], (name, kind, precision, strategy)
+
+
+def test_read_counters_match_reference(il, golden):
+    for name in _names(golden):
+        data, queries, p, eps, G, T = golden_case(golden, name)
+        cfg = il.ExecConfig(group_size=G, tile_size=T, mode="exact")
+        for kind, precision in il.legal_pairs():
+            store = il.build(data, kind, precision)
+            for s in STRATS:
+                il.STRATEGIES[s](store, queries, il.Params(p, eps), cfg)
+            assert store.stats.snapshot() == tuple(golden[f"{name}/{precision.value}/{kind.value}/reads"]), name
+
+
+def test_idw_predict_seq_matches_reference(il, golden):
+    for name in _names(golden):
+        data, queries, p, eps, G, T = golden_case(golden, name)
+        for precision in il.Precision:
+            got = il.idw_predict_seq(data, queries, il.Params(p, eps), precision)
+            ref = golden[f"{name}/{precision.value}/seq"]
+            if p == 2.0:
+                assert np.array_equal(got, ref), (name, precision)
+            else:
+                assert rel(got, ref) <= TOL[precision.value], (name, precision)
+
+
+@pytest.mark.parametrize("strategy", ("naive", "tiled", "nested_improved"))
+def test_fast_mode_within_tolerance_of_truth(il, golden, strategy):
+    for name in _names(golden):
+        data, queries, p, eps, G, T = golden_case(golden, name)
+        cfg = il.ExecConfig(group_size=G, tile_size=T, mode="fast")
+        for kind, precision in il.legal_pairs():
+            store = il.build(data, kind, precision)
+            got = il.STRATEGIES[strategy](store, queries, il.Params(p, eps), cfg)
+            truth = oracle.truth(store, queries, p, eps)
+            assert rel(got, truth) <= TOL[precision.value], (name, kind, precision, strategy)
+
+
+def test_coincidence_exact_all_modes(il):
+    rng = np.random.default_rng(3)
+    data = random_records(rng, 90)
+    data[20] = [data[57][0], data[57][1], 41.0]
+    data[57, 2] = 17.0
+    queries = np.vstack([random_queries(rng, 5), [data[20][:2]]])
+    for mode in ("exact", "fast"):
+        for kind, precision in il.legal_pairs():
+            store = il.build(data, kind, precision)
+            for s, fn in il.STRATEGIES.items():
+                got = fn(store, queries, cfg=il.ExecConfig(group_size=16, tile_size=8, mode=mode))
+                assert float(got[-1]) == float(np.asarray(41.0, precision.dtype)), (mode, kind, s)
+
+
+def test_empty_queries_and_validation(il):
+    store = il.build(random_records(np.random.default_rng(1), 10), il.LayoutKind.SoA, il.Precision.double)
+    for fn in il.STRATEGIES.values():
+        got = fn(store, [], cfg=il.ExecConfig(group_size=4))
+        assert got.shape == (0,)
+        with pytest.raises(ValueError, match="invalid coordinate"):
+            fn(store, [(np.nan, 0.0)])
+    assert store.stats.snapshot() == (0, 0, 0)
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+def test_exact_bitwise_medium_random(il, precision):
+    """n = m = 8192: exact naive/tiled bitwise vs oracle seq, nested vs oracle nested."""
+    rng = np.random.default_rng(11)
+    data = random_records(rng, 8192)
+    queries = random_queries(rng, 8192)
+    prec = il.Precision(precision)
+    store = il.build(data, il.LayoutKind.AoS, prec)
+    ref = oracle.predict(store, queries)
+    for s in ("naive", "tiled"):
+        got = il.STRATEGIES[s](store, queries, cfg=il.ExecConfig(mode="exact"))
+        assert np.array_equal(got, ref), s
+    sub = queries[:512]
+    got = il.run_nested_improved(store, sub, cfg=il.ExecConfig(mode="exact"))
+    assert np.array_equal(got, oracle.nested_improved(store, sub)), "nested_improved"
+
+
+def test_determinism_repeated_runs(il):
+    rng = np.random.default_rng(5)
+    data = random_records(rng, 3000)
+    queries = random_queries(rng, 5000)
+    for mode in ("exact", "fast"):
+        store = il.build(data, il.LayoutKind.AoaS, il.Precision.single)
+        for s, fn in il.STRATEGIES.items():
+            cfg = il.ExecConfig(group_size=64, mode=mode)
+            assert np.array_equal(fn(store, queries, cfg=cfg), fn(store, queries, cfg=cfg)), (mode, s)
+
+
+def test_fast_splits_tolerance(il):
+    """FAST tiled with forced data splits (the skewed-workload path)."""
+    rng = np.random.default_rng(9)
+    data = random_records(rng, 200_000)
+    queries = random_queries(rng, 3000)
+    store = il.build(data, il.LayoutKind.AoaS, il.Precision.single)
+    truth = oracle.truth(store, queries)
+    for splits in (0, 1, 7, 64):
+        got = il.run_tiled(store, queries, cfg=il.ExecConfig(mode="fast", splits=splits))
+        assert rel(got, truth) <= 1e-5, splits
