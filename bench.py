@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""Headline benchmark of the B200 all-pairs IDW hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+
+Workload (default, BASELINE.json north_star): C3 = 1,048,576 data x 1,048,576
+query points, p = 2, fp32, AoaS layout, tiled kernel (K2), FAST mode, inputs
+from the reference's splitmix64 generator (data seed 0, query seed 1).  One
+step = one whole job: broadcast of the data buffers from rank 0 (N > 1), every
+rank's query shard through K2 + fix-up, gather of the predictions.
+
+`value` is whole-job pairs/s with inputs resident in HBM (CUDA events on the
+launching stream, barrier + synchronize on both sides, max over ranks); `e2e`
+is the same metric through the public drop-in API (`run_tiled` on host arrays:
+H2D of store + queries and D2H of the predictions inside the timed region).
+`roofline` relates k_tiled's own device time to the MUFU reciprocal roofline
+measured by a probe kernel on the same GPU; `cpu_baseline` times the oracle's
+C port of the reference loop on this host's cores over a bounded query sample.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port; the reference package itself cannot travel to the GPU box) on
+all host threads, on the same config and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GPairs/s (data×query distance-weights/sec) fp32/fp64 at 1/2/4/8 B200; % of MUFU roofline"
+K = 1024
+CONFIGS = {
+    # name: (n, m, layout, precision, variant, p, description)
+    "c1": (10 * K, 10 * K, "soa", "single", "tiled", 2.0, "C1: 10K x 10K, p=2, fp32, SoA"),
+    "c2": (100 * K, 100 * K, "aoas", "single", "tiled", 2.0, "C2: 100K x 100K, p=2, fp32, AoaS"),
+    "c3": (1024 * K, 1024 * K, "aoas", "single", "tiled", 2.0,
+           "C3: 1M data x 1M queries, p=2, fp32, AoaS, tiled (K2)"),
+    "c4": (1024 * K, 1024 * K, "soa", "double", "nested_improved", 3.5,
+           "C4: 1M x 1M, p=3.5, fp64, SoA, split-reduce (K3)"),
+    "c5": (10240 * K, 100 * K, "aoas", "single", "tiled", 2.0,
+           "C5: 10M data x 100K queries, p=2, fp32, AoaS, tiled (K2, data splits)"),
+}
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+SHARD_ALIGN = 256
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--mode", choices=("fast", "exact"), default="fast")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.lines: list[str] = []
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", gpu_id, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------------------
+def make_inputs(cfg_name):
+    import numpy as np
+
+    import paper_1402_4986_b200 as il
+
+    n, m, layout, prec, variant, p, desc = CONFIGS[cfg_name]
+    x, y, z = il.generate_cloud_arrays(n, 0)
+    qx, qy, _ = il.generate_cloud_arrays(m, il.query_seed(0))
+    store = il.LayoutStore.from_arrays(x, y, z, il.LayoutKind(layout), il.Precision(prec))
+    return store, np.column_stack([qx, qy])
+
+
+def cpu_sample(store, queries, p, seconds: float, threads: int):
+    """Time the oracle port (run_naive semantics, all host threads) on a
+    bounded query sample sized for ~`seconds` of CPU work."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle
+
+    n = store.count
+    m0 = max(threads * 16, 64)
+    t0 = time.perf_counter()
+    oracle.predict_mt(store, queries[:m0], p, threads=threads)
+    dt0 = max(time.perf_counter() - t0, 1e-6)
+    msub = int(min(queries.shape[0], max(m0, m0 * seconds / dt0)))
+    msub = max(threads, (msub // threads) * threads)
+    t1 = time.perf_counter()
+    oracle.predict_mt(store, queries[:msub], p, threads=threads)
+    dt = time.perf_counter() - t1
+    return n * msub / dt / 1e9, msub, dt
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host CPU (oracle port)."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle
+
+    n, m, layout, prec, variant, p, desc = CONFIGS[args.config]
+    store, queries = make_inputs(args.config)
+    threads = oracle.max_threads()
+    # size one step for ~6 s of CPU work
+    m0 = threads * 16
+    t0 = time.perf_counter()
+    oracle.predict_mt(store, queries[:m0], p, threads=threads)
+    per_q = max(time.perf_counter() - t0, 1e-6) / m0
+    msub = max(threads, int(6.0 / per_q) // threads * threads)
+    msub = min(msub, m)
+    for _ in range(args.warmup):
+        oracle.predict_mt(store, queries[:msub], p, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        oracle.predict_mt(store, queries[:msub], p, threads=threads)
+        times.append(time.perf_counter() - t)
+    tot = sum(times)
+    value = n * msub * args.steps / tot / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GPairs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32" if prec == "single" else "f64", "data": "synthetic splitmix64 (generate_cloud_arrays seeds 0/1)",
+        "config": {"workload": desc, "n": n, "m": m, "layout": layout, "precision": prec, "variant": "naive (CPU)",
+                   "p": p, "sample_queries_per_step": msub},
+        "cpu_baseline": {"value": value, "unit": "GPairs/s", "cores": threads, "kind": "port",
+                         "sample": f"{n} data x {msub} queries per step (oracle/idw_oracle.c predict_block, "
+                                   f"{threads} pthreads, 256-query blocks)"},
+        "e2e": {"value": value, "unit": "GPairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_1402_4986_b200 as il
+    from paper_1402_4986_b200 import _capi
+    from paper_1402_4986_b200.device import DeviceStore, predict_device
+    from paper_1402_4986_b200.partition import QueryShardedRunner, StoreMeta, shard_bounds
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    n, m, layout, prec, variant, p, desc = CONFIGS[args.config]
+    params = il.Params(p)
+    cfg = il.ExecConfig(mode=args.mode, device=local)
+    tdt = torch.float32 if prec == "single" else torch.float64
+
+    # ---- inputs: data built on rank 0 and replicated by broadcast; each rank
+    # holds its query shard in HBM before the timed region starts.
+    store, queries = make_inputs(args.config) if rank == 0 or world == 1 else (None, None)
+    if queries is None:
+        qx64, qy64, _ = il.generate_cloud_arrays(m, il.query_seed(0))
+        queries = np.column_stack([qx64, qy64])
+    lo, hi = shard_bounds(m, world, rank, SHARD_ALIGN)
+    npdt = np.float32 if prec == "single" else np.float64
+    qx_l = torch.from_numpy(np.ascontiguousarray(queries[lo:hi, 0].astype(npdt))).to(dev)
+    qy_l = torch.from_numpy(np.ascontiguousarray(queries[lo:hi, 1].astype(npdt))).to(dev)
+    out_l = torch.empty(hi - lo, dtype=tdt, device=dev)
+
+    if world > 1:
+        runner = QueryShardedRunner(dist, dev, align=SHARD_ALIGN)
+        meta = StoreMeta(layout, prec, n, [b.nbytes for b in store.buffers]) if rank == 0 else None
+        meta = runner.broadcast_meta(meta)
+        src_bufs = DeviceStore(store, local).tensors if rank == 0 else None
+        bufs = runner.broadcast_buffers(src_bufs, meta)
+        dstore = DeviceStore.from_tensors(il.LayoutKind(layout), il.Precision(prec), n, bufs, meta.nbytes, local)
+    else:
+        runner = None
+        dstore = DeviceStore(store, local)
+        bufs = dstore.tensors
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    launches = [0]
+
+    def step(record=None):
+        if runner is not None:
+            for t in bufs:  # the data replication collective (NVLink/NVSwitch)
+                dist.broadcast(t, src=0)
+        st = predict_device(dstore, qx_l, qy_l, out_l, params, cfg, variant, stream)
+        launches[0] += int(st.kernel_launches)
+        if record is not None:
+            record.append(_capi.last_kernel_ms())
+        if runner is not None:
+            runner.gather(out_l, m)
+        flush.zero_()  # L2 flush between steps (256 MiB > 126 MB L2)
+
+    # ---- MUFU roofline probe (same GPU, just before the timed region)
+    probe_rate, probe_hz = _capi.mufu_peak(local)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    props = torch.cuda.get_device_properties(dev)
+    gpu_id = str(getattr(props, "uuid", local))
+    if gpu_id and not gpu_id.startswith("GPU-") and len(gpu_id) == 36:
+        gpu_id = "GPU-" + gpu_id
+    sampler = ClockSampler(gpu_id)
+    time.sleep(0.3)
+    launches[0] = 0
+    kern = []
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(kern)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms_local = e0.elapsed_time(e1)
+    ms = ms_local
+    if dist is not None:
+        t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_pairs = float(n) * float(m)
+    value = total_pairs * args.steps / (ms * 1e-3) / 1e9
+    ms_step = ms / args.steps
+
+    # ---- roofline of the dominant kernel (k_tiled / k_nested), this rank
+    kmain = statistics.mean(k[0] for k in kern)
+    kfix = statistics.mean(k[1] for k in kern)
+    pairs_launch = float(n) * float(hi - lo)
+    achieved = pairs_launch / (kmain * 1e-3) / 1e9
+    sms = props.multi_processor_count
+    mufu_per_pair = 1 if p == 2.0 else 2
+    run_clock_peak = None
+    if clocks.get("sm_mhz"):
+        run_clock_peak = sms * 16 * clocks["sm_mhz"] * 1e6 / mufu_per_pair / 1e9
+    roof = {
+        "bound": "mufu" if prec == "single" else "fp64",
+        "achieved": achieved,
+        "peak": probe_rate / mufu_per_pair / 1e9,
+        "unit": "GPairs/s",
+        "frac": achieved / (probe_rate / mufu_per_pair / 1e9),
+        "traffic": None,
+        "kernel": "k_tiled" if variant == "tiled" else "k_nested",
+        "kernel_ms": kmain,
+        "fixup_ms": kfix,
+        "peak_source": "measured: idw_mufu_peak probe (rcp.approx chains on all SMs) in this run, "
+                       f"{probe_hz / 1e6:.0f} MHz implied; 16 MUFU lanes/clk/SM x {sms} SMs",
+        "peak_at_run_clock": run_clock_peak,
+        "frac_at_run_clock": achieved / run_clock_peak if run_clock_peak else None,
+        "algorithmic_unit": "one (query, data) pair = 1 rcp + 2 sums; n*m_shard pairs per launch",
+    }
+    if prec == "double":
+        roof["note"] = "fp64 kernels are FP64-pipe bound; the MUFU figure is only a reference line"
+
+    # ---- e2e through the public drop-in API (host buffers, blocking)
+    e2e = None
+    if not args.no_e2e:
+        fn = il.STRATEGIES[variant]
+        local_store = store
+        if local_store is None:  # non-source ranks rebuild their host copy from HBM
+            raw = [t[:nb].cpu().numpy() for t, nb in zip(bufs, meta.nbytes)]
+            local_store = il.LayoutStore(il.LayoutKind(layout), il.Precision(prec), n, raw,
+                                         il.buffer_shapes(il.LayoutKind(layout), il.Precision(prec), n))
+        # pinned host copies of the store buffers (inputs of every step)
+        pinned = []
+        for b in local_store.buffers:
+            t = torch.empty(b.nbytes, dtype=torch.uint8, pin_memory=True)
+            t.numpy()[:] = b
+            pinned.append(t.numpy())
+        hstore = il.LayoutStore(local_store.kind, local_store.precision, n, pinned, local_store.shapes)
+        hq = np.ascontiguousarray(queries[lo:hi])
+        for _ in range(min(args.warmup, 2)):
+            fn(hstore, hq, params, cfg)
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res = fn(hstore, hq, params, cfg)
+        t_e2e = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        e = 4 if prec == "single" else 8
+        h2d = sum(b.nbytes for b in hstore.buffers) + 2 * (hi - lo) * e
+        d2h = (hi - lo) * e
+        h2d_all, d2h_all = h2d, d2h
+        if dist is not None:
+            t = torch.tensor([h2d, d2h], device=dev, dtype=torch.float64)
+            dist.all_reduce(t)
+            h2d_all, d2h_all = int(t[0].item()), int(t[1].item())
+        e2e = {"value": total_pairs * args.steps / t_e2e / 1e9, "unit": "GPairs/s",
+               "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": int(d2h_all),
+               "api": f"paper_1402_4986_b200.{fn.__name__}(LayoutStore[pinned host], queries[host f64], "
+                      f"Params(p={p}), ExecConfig(mode='{args.mode}'))"}
+        del res
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle
+
+        threads = oracle.max_threads()
+        v, msub, dt = cpu_sample(store, queries, p, args.cpu_seconds, threads)
+        cpu = {"value": v, "unit": "GPairs/s", "cores": threads, "kind": "port",
+               "sample": f"{n} data x {msub} queries ({dt:.1f} s), oracle/idw_oracle.c predict_block "
+                         f"(reference kernels.py:34-67 restated in C), {threads} pthreads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GPairs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32" if prec == "single" else "f64",
+            "data": "synthetic: splitmix64 uniform cloud (idwlayout generate_cloud_arrays, data seed 0, "
+                    "query seed 1), x,y in [0,1), z in [0,100)",
+            "config": {"workload": desc, "n": n, "m": m, "layout": layout, "precision": prec,
+                       "variant": variant, "mode": args.mode, "p": p, "zero_eps": 0.0,
+                       "parallelism": f"query-shard x{world} (data broadcast + gather per step)",
+                       "l2": "flushed between steps (256 MiB write); inputs resident in HBM"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches[0],
+            "mufu_probe": {"rcp_per_s": probe_rate, "sm_mhz": probe_hz / 1e6},
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

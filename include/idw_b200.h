@@ -130,6 +130,11 @@ int idw_run(const idw_store *store, const void *qx, const void *qy, int64_t m,
 int idw_run_device(const idw_store *store, const void *qx, const void *qy, int64_t m,
                    const idw_params *prm, void *out, void *stream, idw_stats *stats);
 
+/* Device time of the last successful idw_run_device call on this thread:
+ * the variant kernels (e.g. k_tiled [+ k_combine]) and the FAST fix-up pass,
+ * from events recorded on the call's stream.  Blocks until they complete.   */
+int idw_last_kernel_ms(double *variant_ms, double *fixup_ms);
+
 /* Measured MUFU reciprocal rate of `device`: a register-resident loop of
  * independent rcp.approx.f32 over all SMs, timed with events.  Writes
  * rcp results per second (== the p = 2 fp32 pair roofline) and the mean SM

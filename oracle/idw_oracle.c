@@ -314,6 +314,10 @@ static void *mt_worker(void *arg) {
 static void mt_run(mt_job *j, int threads) {
   if (threads < 1) threads = 1;
   if (threads > 1024) threads = 1024;
+  /* shrink blocks when m is small so every thread gets work (results do not
+   * depend on the block size: each query is computed independently) */
+  const int64_t fair = j->m / ((int64_t)threads * 8);
+  if (fair < j->block) j->block = fair > 1 ? fair : 1;
   atomic_init(&j->next, 0);
   pthread_t tid[1024];
   int started = 0;

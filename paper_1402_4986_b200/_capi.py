@@ -61,7 +61,7 @@ class IdwStats(ctypes.Structure):
 
 
 EXPORTS = ("idw_abi_version", "idw_device_count", "idw_last_error", "idw_run",
-           "idw_run_device", "idw_mufu_peak")
+           "idw_run_device", "idw_last_kernel_ms", "idw_mufu_peak")
 
 
 class NativeError(RuntimeError):
@@ -104,6 +104,8 @@ def load() -> ctypes.CDLL:
     lib.idw_run_device.restype = ctypes.c_int
     lib.idw_run_device.argtypes = [ctypes.POINTER(IdwStore), ptr, ptr, ctypes.c_int64,
                                    ctypes.POINTER(IdwParams), ptr, ptr, ctypes.POINTER(IdwStats)]
+    lib.idw_last_kernel_ms.restype = ctypes.c_int
+    lib.idw_last_kernel_ms.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
     lib.idw_mufu_peak.restype = ctypes.c_int
     lib.idw_mufu_peak.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double)]
@@ -166,6 +168,14 @@ def run_device(store: IdwStore, qx_ptr: int, qy_ptr: int, m: int, params: IdwPar
     _check(lib.idw_run_device(ctypes.byref(store), qx_ptr, qy_ptr, m, ctypes.byref(params),
                               out_ptr, stream, ctypes.byref(stats)))
     return stats
+
+
+def last_kernel_ms() -> tuple[float, float]:
+    """(variant kernels ms, fix-up ms) of this thread's last run_device call."""
+    a = ctypes.c_double()
+    b = ctypes.c_double()
+    _check(load().idw_last_kernel_ms(ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def mufu_peak(device: int = 0) -> tuple[float, float]:

@@ -24,7 +24,9 @@ static __global__ void k_mufu_probe(float *out, int iters, unsigned long long *c
   long long c0 = clock64();
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(a[k]));
+    // rcp then +1: not an involution, so ptxas cannot fold pairs of MUFU.RCP
+    for (int k = 0; k < 8; ++k)
+      asm volatile("{ rcp.approx.ftz.f32 %0, %0;\n\t add.ftz.f32 %0, %0, 0f3F800000; }" : "+f"(a[k]));
   }
   long long c1 = clock64();
   float s = 0.f;
@@ -129,8 +131,17 @@ static void fill_launch(Launch &L, const idw_store *s, const void *const *bufs, 
   L.out = out;
 }
 
-static int dispatch(Launch &L) {
+// Events bracketing the variant kernels and the fix-up pass of the last
+// idw_run_device call on this thread (read back by idw_last_kernel_ms).
+struct EvSet {
+  cudaEvent_t a = nullptr, b = nullptr, c = nullptr;
+};
+static thread_local EvSet g_ev[64];
+static thread_local int g_last_dev = -1;
+
+static int dispatch(Launch &L, const EvSet *ev = nullptr) {
   int rc = 0;
+  if (ev) IDW_CK(cudaEventRecord(ev->a, L.st));
   switch (L.variant) {
     case IDW_NAIVE: rc = launch_naive(L); break;
     case IDW_TILED: rc = launch_tiled(L); break;
@@ -139,7 +150,10 @@ static int dispatch(Launch &L) {
     default: set_error("unknown variant"); return IDW_E_ARG;
   }
   if (rc) return rc;
+  if (ev) IDW_CK(cudaEventRecord(ev->b, L.st));
   if (L.mode == IDW_FAST && L.variant != IDW_NESTED_ORIGINAL) rc = launch_fixup(L);
+  if (rc) return rc;
+  if (ev) IDW_CK(cudaEventRecord(ev->c, L.st));
   return rc;
 }
 
@@ -187,7 +201,14 @@ int idw_run_device(const idw_store *s, const void *qx, const void *qy, int64_t m
     IDW_CK(cudaMallocAsync((void **)&flags, (size_t)m, L.st));
     L.flags = flags;
   }
-  rc = dispatch(L);
+  EvSet &ev = g_ev[p->device];
+  if (!ev.a) {
+    IDW_CK(cudaEventCreate(&ev.a));
+    IDW_CK(cudaEventCreate(&ev.b));
+    IDW_CK(cudaEventCreate(&ev.c));
+  }
+  rc = dispatch(L, &ev);
+  g_last_dev = rc == 0 ? p->device : -1;
   if (flags) cudaFreeAsync(flags, L.st);
   fill_stats(stats, L, p, s->count, m);
   return rc;
@@ -258,6 +279,20 @@ int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const
   cudaEventDestroy(e1);
   fill_stats(stats, L, p, s->count, m);
   return rc;
+}
+
+int idw_last_kernel_ms(double *variant_ms, double *fixup_ms) {
+  g_err.clear();
+  if (g_last_dev < 0) return set_error("no completed idw_run_device call on this thread"), IDW_E_ARG;
+  EvSet &ev = g_ev[g_last_dev];
+  IDW_CK(cudaSetDevice(g_last_dev));
+  IDW_CK(cudaEventSynchronize(ev.c));
+  float a = 0.f, b = 0.f;
+  IDW_CK(cudaEventElapsedTime(&a, ev.a, ev.b));
+  IDW_CK(cudaEventElapsedTime(&b, ev.b, ev.c));
+  if (variant_ms) *variant_ms = a;
+  if (fixup_ms) *fixup_ms = b;
+  return 0;
 }
 
 int idw_mufu_peak(int device, double *rcp_per_s, double *sm_hz) {
