@@ -304,7 +304,10 @@ int idw_mufu_peak(int device, double *rcp_per_s, double *sm_hz) {
   unsigned long long *dcyc = nullptr;
   IDW_CK(cudaMallocAsync((void **)&dout, 16, st));
   IDW_CK(cudaMallocAsync((void **)&dcyc, 16, st));
-  const int blocks = sms * 8, threads = 256, iters = 8192;
+  // one resident wave: block 0's clock64 span then equals the kernel span
+  int per_sm = 0;
+  IDW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mufu_probe, 256, 0));
+  const int blocks = sms * (per_sm > 0 ? per_sm : 1), threads = 256, iters = 8192;
   cudaEvent_t e0, e1;
   IDW_CK(cudaEventCreate(&e0));
   IDW_CK(cudaEventCreate(&e1));

@@ -17,25 +17,65 @@ namespace idw {
 
 template <typename T, int MODE>
 struct TiledCfg;
-// fp32: 1024-point tiles; FAST packs 8 queries (4 pairs) per thread.
+// fp32: 256-point warp tiles; FAST packs 8 queries (4 pairs) per thread.
 template <>
 struct TiledCfg<float, FAST> {
-  static constexpr int Q = 8, TILE = 1024, NC_MAX = 256;
+  static constexpr int Q = 8, TILE = 256, NC_MAX = 256;
 };
 template <>
 struct TiledCfg<float, EXACT> {
-  static constexpr int Q = 4, TILE = 1024, NC_MAX = 256;
+  static constexpr int Q = 4, TILE = 256, NC_MAX = 256;
 };
 template <>
 struct TiledCfg<double, FAST> {
-  static constexpr int Q = 4, TILE = 512, NC_MAX = 256;
+  static constexpr int Q = 4, TILE = 128, NC_MAX = 256;
 };
 template <>
 struct TiledCfg<double, EXACT> {
-  static constexpr int Q = 2, TILE = 512, NC_MAX = 256;
+  static constexpr int Q = 2, TILE = 128, NC_MAX = 256;
 };
 
 static inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+
+// Choose (query block size, data splits) so that blocks x splits fills the
+// resident slots in whole waves: every CTA costs qpc x tiles_per_split pair
+// units, and the search minimises waves x that cost (ties -> fewer splits).
+// Query blocks keep >= 4 warps busy unless m itself is smaller.
+struct Shape {
+  long long qpc, blocks, splits, tps;
+};
+static Shape shape_grid(long long m, long long ntiles, long long slots, int Q, int nc_max, bool allow_split,
+                        int forced_splits) {
+  const long long cap = (long long)nc_max * Q;
+  const long long min_q = std::min<long long>(cap / 2, cdiv(m, Q) * Q);
+  Shape best{0, 0, 0, 0};
+  double best_cost = 0;
+  const long long smax = allow_split ? std::min<long long>(ntiles, 256) : 1;
+  for (long long S = 1; S <= smax; ++S) {
+    if (forced_splits > 0 && S != std::min<long long>(forced_splits, ntiles)) continue;
+    const long long tps = cdiv(ntiles, S);
+    const long long splits = cdiv(ntiles, tps);
+    for (long long W = 1; W <= 64; ++W) {
+      long long blocks = std::max<long long>(1, (W * slots) / splits);
+      long long qpc = cdiv(cdiv(m, blocks), Q) * Q;
+      if (qpc > cap) continue;  // too few blocks for this many waves
+      if (qpc < min_q) break;   // more waves only shrink blocks further
+      blocks = cdiv(m, qpc);
+      const long long waves = cdiv(blocks * splits, slots);
+      const double cost = (double)waves * (double)qpc * (double)tps;
+      if (best.qpc == 0 || cost < best_cost * 0.999) {
+        best = {qpc, blocks, splits, tps};
+        best_cost = cost;
+      }
+      break;  // smallest feasible W for this S is the one to take
+    }
+  }
+  if (best.qpc == 0) {  // fall back: full blocks, no split
+    const long long qpc = std::min<long long>(cap, cdiv(m, Q) * Q);
+    best = {qpc, cdiv(m, qpc), 1, ntiles};
+  }
+  return best;
+}
 
 int launch_tiled(Launch &L) {
   return with_layout(L, [&](auto KC, auto tv) -> int {
@@ -46,43 +86,23 @@ int launch_tiled(Launch &L) {
       constexpr bool P2 = decltype(PC)::value, EPS = decltype(EC)::value;
       using C = TiledCfg<T, MODE>;
       constexpr int Q = C::Q, TILE = C::TILE;
+      constexpr int RING = tiled_ring_bytes<K, T, TILE>();
       auto kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE>;
-      const int smem = tiled_smem_bytes<K, T, TILE>();
-      IDW_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      const int smem_max = (C::NC_MAX / 32) * RING;
+      IDW_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
       int occ = 0;
-      IDW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NC_MAX + 32, smem));
+      IDW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NC_MAX, smem_max));
       if (occ < 1) occ = 1;
       const long long slots = (long long)L.sms * occ;
       const long long ntiles = cdiv(L.n, TILE);
-      const long long cap = (long long)C::NC_MAX * Q;
-      long long blocks = cdiv(L.m, cap);
-      long long splits = 1;
-      if (MODE == FAST) {
-        if (L.splits > 0) {
-          splits = L.splits;
-        } else if (blocks < slots) {
-          splits = std::max<long long>(1, slots / blocks);
-        }
-        splits = std::min(splits, ntiles);
-      }
-      long long qpc;
-      if (blocks >= slots) {
-        const long long waves = cdiv(blocks, slots);
-        blocks = waves * slots;
-        qpc = cdiv(L.m, blocks);
-        qpc = cdiv(qpc, Q) * Q;
-      } else {
-        qpc = std::min<long long>(cap, cdiv(L.m, Q) * Q);
-      }
-      blocks = cdiv(L.m, qpc);
-      int nc = (int)cdiv(cdiv(qpc, Q), 32) * 32;
-      const long long tps = cdiv(ntiles, splits);
-      splits = cdiv(ntiles, tps);
+      const Shape sh = shape_grid(L.m, ntiles, slots, Q, C::NC_MAX, MODE == FAST, L.splits);
+      const int nc = (int)cdiv(cdiv(sh.qpc, Q), 32) * 32;
+      const int smem = (nc / 32) * RING;
 
       SplitOut<T> so{nullptr, nullptr, nullptr, nullptr, nullptr};
       void *ws = nullptr;
-      if (splits > 1) {
-        const size_t per = (size_t)splits * (size_t)L.m;
+      if (sh.splits > 1) {
+        const size_t per = (size_t)sh.splits * (size_t)L.m;
         IDW_CK(cudaMallocAsync(&ws, per * (4 * sizeof(T) + 1), L.st));
         T *base = (T *)ws;
         so.shi = base;
@@ -91,14 +111,14 @@ int launch_tiled(Launch &L) {
         so.zlo = base + 3 * per;
         so.flag = (unsigned char *)(base + 4 * per);
       }
-      dim3 grid((unsigned)blocks, (unsigned)splits);
-      kern<<<grid, nc + 32, smem, L.st>>>(L.g, L.n, (const T *)L.qx, (const T *)L.qy, L.m, qpc, tps,
-                                          make_scal<T>(L), (T *)L.out, L.flags, so);
+      dim3 grid((unsigned)sh.blocks, (unsigned)sh.splits);
+      kern<<<grid, nc, smem, L.st>>>(L.g, L.n, (const T *)L.qx, (const T *)L.qy, L.m, sh.qpc, sh.tps,
+                                     make_scal<T>(L), (T *)L.out, L.flags, so);
       IDW_CK_LAUNCH();
       ++L.launches;
-      if (splits > 1) {
+      if (sh.splits > 1) {
         if constexpr (MODE == FAST) {
-          k_combine<T><<<(unsigned)cdiv(L.m, 256), 256, 0, L.st>>>(L.m, (int)splits, so, (T)L.eps_flag,
+          k_combine<T><<<(unsigned)cdiv(L.m, 256), 256, 0, L.st>>>(L.m, (int)sh.splits, so, (T)L.eps_flag,
                                                                    (T *)L.out, L.flags);
           IDW_CK_LAUNCH();
           ++L.launches;
