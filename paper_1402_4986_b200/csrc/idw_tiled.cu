@@ -9,6 +9,7 @@
 // FAST runs with too few queries to fill the slots also split the data range
 // (blockIdx.y) and fold the per-split partials in split order (k_combine).
 #include <algorithm>
+#include <cstdlib>
 
 #include "idw_kernels.cuh"
 #include "idw_launch.h"
@@ -88,6 +89,14 @@ int launch_tiled(Launch &L) {
       constexpr int Q = C::Q, TILE = C::TILE;
       constexpr int RING = tiled_ring_bytes<K, T, TILE>();
       auto kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE>;
+      if constexpr (std::is_same<T, float>::value && MODE == FAST && P2 && !EPS) {
+        // One of the four packed query pairs per point shares a reciprocal
+        // (measured on C3: 0 -> 4196, 1 -> 4546, 2 -> 4533 GPairs/s; the mix of
+        // MUFU and FMA-pipe work is best balanced at 1).  IDW_PROD overrides.
+        static const int prod = [] { const char *e = getenv("IDW_PROD"); return e ? atoi(e) : 1; }();
+        if (prod == 1) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 1>;
+        if (prod == 2) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 2>;
+      }
       const int smem_max = (C::NC_MAX / 32) * RING;
       IDW_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
       int occ = 0;

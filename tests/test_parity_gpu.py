@@ -151,3 +151,39 @@ def test_fast_splits_tolerance(il):
     for splits in (0, 1, 7, 64):
         got = il.run_tiled(store, queries, cfg=il.ExecConfig(mode="fast", splits=splits))
         assert rel(got, truth) <= 1e-5, splits
+
+
+@pytest.mark.parametrize("scale", [1e-18, 1e-3, 1.0, 1e4, 1e10, 1e15])
+def test_fast_coordinate_scales(il, scale):
+    """FAST fp32 over clouds scaled to extreme ranges: the shared-reciprocal
+    guard must fall back when a*b could overflow (large scales), and underflow
+    (tiny scales) must be screened and fixed up -- always within tolerance."""
+    rng = np.random.default_rng(17)
+    data = random_records(rng, 5000)
+    data[:, :2] *= scale
+    queries = random_queries(rng, 3000) * scale
+    store = il.build(data, il.LayoutKind.AoaS, il.Precision.single)
+    truth = oracle.truth(store, queries)
+    for s in ("tiled", "naive", "nested_improved"):
+        got = il.STRATEGIES[s](store, queries, cfg=il.ExecConfig(mode="fast"))
+        assert np.all(np.isfinite(got)), (scale, s)
+        assert rel(got, truth) <= 1e-5, (scale, s)
+
+
+def test_fast_queries_on_data_points(il):
+    """Every query coincides with a data point: all queries go through the
+    exact fix-up and must return that point's z exactly."""
+    rng = np.random.default_rng(23)
+    data = random_records(rng, 4000)
+    idx = rng.choice(4000, size=700, replace=False)
+    queries = data[idx, :2]
+    for precision in il.Precision:
+        store = il.build(data, il.LayoutKind.SoA, precision)
+        zs = store.to_arrays()[2]
+        ref = oracle.predict(store, queries)
+        for s in ("tiled", "naive", "nested_improved"):
+            st = il.RunStats()
+            got = il.STRATEGIES[s](store, queries, cfg=il.ExecConfig(mode="fast"), instrumentation=st)
+            assert np.array_equal(got, ref), (precision, s)
+            assert np.array_equal(got, zs[idx]), (precision, s)
+            assert st.fixup_queries == len(idx), (precision, s)
