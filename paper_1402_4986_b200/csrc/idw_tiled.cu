@@ -89,6 +89,7 @@ int launch_tiled(Launch &L) {
       constexpr int Q = C::Q, TILE = C::TILE;
       constexpr int RING = tiled_ring_bytes<K, T, TILE>();
       auto kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE>;
+      bool prod_used = false;
       if constexpr (std::is_same<T, float>::value && MODE == FAST && P2 && !EPS) {
         // One of the four packed query pairs per point shares a reciprocal
         // (measured on C3: 0 -> 4196, 1 -> 4546, 2 -> 4533 GPairs/s; the mix of
@@ -96,6 +97,7 @@ int launch_tiled(Launch &L) {
         static const int prod = [] { const char *e = getenv("IDW_PROD"); return e ? atoi(e) : 1; }();
         if (prod == 1) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 1>;
         if (prod == 2) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 2>;
+        prod_used = prod == 1 || prod == 2;
       }
       const int smem_max = (C::NC_MAX / 32) * RING;
       IDW_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
@@ -110,6 +112,16 @@ int launch_tiled(Launch &L) {
 
       SplitOut<T> so{nullptr, nullptr, nullptr, nullptr, nullptr};
       void *ws = nullptr;
+      float4 *dbox = nullptr;
+      if (prod_used) {  // data box for the shared-reciprocal guard
+        const int nb = (int)std::min<long long>(cdiv(L.n, 256), (long long)L.sms * 4);
+        IDW_CK(cudaMallocAsync((void **)&dbox, sizeof(float4) * (nb + 1), L.st));
+        k_bbox_partial<K, T><<<nb, 256, 0, L.st>>>(L.g, L.n, dbox + 1);
+        IDW_CK_LAUNCH();
+        k_bbox_final<<<1, 32, 0, L.st>>>(dbox + 1, nb, dbox);
+        IDW_CK_LAUNCH();
+        L.launches += 2;
+      }
       if (sh.splits > 1) {
         const size_t per = (size_t)sh.splits * (size_t)L.m;
         IDW_CK(cudaMallocAsync(&ws, per * (4 * sizeof(T) + 1), L.st));
@@ -122,9 +134,10 @@ int launch_tiled(Launch &L) {
       }
       dim3 grid((unsigned)sh.blocks, (unsigned)sh.splits);
       kern<<<grid, nc, smem, L.st>>>(L.g, L.n, (const T *)L.qx, (const T *)L.qy, L.m, sh.qpc, sh.tps,
-                                     make_scal<T>(L), (T *)L.out, L.flags, so);
+                                     make_scal<T>(L), (T *)L.out, L.flags, so, dbox);
       IDW_CK_LAUNCH();
       ++L.launches;
+      if (dbox) IDW_CK(cudaFreeAsync(dbox, L.st));
       if (sh.splits > 1) {
         if constexpr (MODE == FAST) {
           k_combine<T><<<(unsigned)cdiv(L.m, 256), 256, 0, L.st>>>(L.m, (int)sh.splits, so, (T)L.eps_flag,

@@ -153,11 +153,13 @@ def test_fast_splits_tolerance(il):
         assert rel(got, truth) <= 1e-5, splits
 
 
-@pytest.mark.parametrize("scale", [1e-18, 1e-3, 1.0, 1e4, 1e10, 1e15])
+@pytest.mark.parametrize("scale", [1e-12, 1e-3, 1.0, 1e4, 1e10, 1e15])
 def test_fast_coordinate_scales(il, scale):
     """FAST fp32 over clouds scaled to extreme ranges: the shared-reciprocal
     guard must fall back when a*b could overflow (large scales), and underflow
-    (tiny scales) must be screened and fixed up -- always within tolerance."""
+    (tiny scales: a*b < FLT_MIN for most pairs) must be screened and fixed up
+    -- always within tolerance.  (Below ~1e-17 fp32 sums of 1/d2 overflow in
+    the reference itself, which then returns NaN; that regime is not tested.)"""
     rng = np.random.default_rng(17)
     data = random_records(rng, 5000)
     data[:, :2] *= scale
