@@ -92,6 +92,8 @@ inline Scal<T> make_scal(const Launch &L) {
   s.eps = (T)L.eps;
   s.wexp = (T)L.wexp;
   s.eps_flag = (T)L.eps_flag;
+  const double twop = -4.0 * L.wexp;  // 2p (wexp = -p/2)
+  s.jq = (!L.p2 && twop == (double)(long long)twop && twop >= 1.0 && twop <= 64.0) ? (int)twop : 0;
   return s;
 }
 

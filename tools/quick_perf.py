@@ -27,6 +27,12 @@ def run(n, m, kind, prec, variant, mode, p=2.0, reps=3, G=1024, splits=0):
     print(json.dumps(r), flush=True)
     return out
 
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "nested":
+    K = 1024
+    run(1024 * K, 64 * K, "soa", "double", "nested_improved", "fast", p=3.5, reps=2)
+    run(102400, 102400, "soa", "double", "nested_improved", "fast", p=2.0, reps=2)
+    run(10240 * K, 100 * K, "aoas", "single", "nested_improved", "fast", reps=2)
+    sys.exit(0)
 if __name__ == "__main__":
     rate, hz = il._capi.mufu_peak(0)
     print(json.dumps(dict(mufu_rcp_per_s=rate, pairs_roofline_gpairs=rate / 1e9, sm_hz=hz)), flush=True)
