@@ -151,7 +151,7 @@ static int dispatch(Launch &L, const EvSet *ev = nullptr) {
   }
   if (rc) return rc;
   if (ev) IDW_CK(cudaEventRecord(ev->b, L.st));
-  if (L.mode == IDW_FAST && L.variant != IDW_NESTED_ORIGINAL) rc = launch_fixup(L);
+  if (needs_fixup(L)) rc = launch_fixup(L);
   if (rc) return rc;
   if (ev) IDW_CK(cudaEventRecord(ev->c, L.st));
   return rc;
@@ -197,7 +197,7 @@ int idw_run_device(const idw_store *s, const void *qx, const void *qy, int64_t m
   L.dev = p->device;
   L.sms = sms;
   unsigned char *flags = nullptr;
-  if (p->mode == IDW_FAST) {
+  if (needs_fixup(L)) {
     IDW_CK(cudaMallocAsync((void **)&flags, (size_t)m, L.st));
     L.flags = flags;
   }
@@ -253,7 +253,7 @@ int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const
   L.st = st;
   L.dev = p->device;
   L.sms = sms;
-  if (p->mode == IDW_FAST) L.flags = arena + off[6];
+  if (needs_fixup(L)) L.flags = arena + off[6];
   L.nfixed = (unsigned long long *)(arena + off[7]);
   cudaEvent_t e0, e1;
   IDW_CK(cudaEventCreate(&e0));

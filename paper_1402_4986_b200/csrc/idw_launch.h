@@ -77,11 +77,14 @@ int with_layout(const Launch &L, F &&f) {
   }
 }
 
-// Visit (mode, p == 2, zero_eps > 0).  EXACT always tests coincidence in the
-// loop, so only FAST distinguishes the eps flag.
+// Visit (mode, p == 2, zero_eps > 0).  EXACT with zero_eps > 0 keeps the
+// per-pair coincidence bookkeeping; with zero_eps == 0 naive/tiled screen.
 template <class F>
 int with_arith(const Launch &L, F &&f) {
-  if (L.mode == EXACT) return L.p2 ? f(IC<EXACT>{}, BC<true>{}, BC<false>{}) : f(IC<EXACT>{}, BC<false>{}, BC<false>{});
+  if (L.mode == EXACT) {
+    if (L.p2) return L.epsp ? f(IC<EXACT>{}, BC<true>{}, BC<true>{}) : f(IC<EXACT>{}, BC<true>{}, BC<false>{});
+    return L.epsp ? f(IC<EXACT>{}, BC<false>{}, BC<true>{}) : f(IC<EXACT>{}, BC<false>{}, BC<false>{});
+  }
   if (L.p2) return L.epsp ? f(IC<FAST>{}, BC<true>{}, BC<true>{}) : f(IC<FAST>{}, BC<true>{}, BC<false>{});
   return L.epsp ? f(IC<FAST>{}, BC<false>{}, BC<true>{}) : f(IC<FAST>{}, BC<false>{}, BC<false>{});
 }
@@ -103,5 +106,12 @@ int launch_tiled(Launch &L);
 int launch_nested(Launch &L);
 int launch_nested_orig(Launch &L);
 int launch_fixup(Launch &L);
+
+// Does this launch write screen flags and need the fix-up pass?
+inline bool needs_fixup(const Launch &L) {
+  if (L.variant == IDW_NESTED_ORIGINAL) return false;
+  if (L.mode == FAST) return true;
+  return !L.epsp && (L.variant == IDW_NAIVE || L.variant == IDW_TILED);  // screened EXACT
+}
 
 }  // namespace idw

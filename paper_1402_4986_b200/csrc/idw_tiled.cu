@@ -113,7 +113,9 @@ int launch_tiled(Launch &L) {
       SplitOut<T> so{nullptr, nullptr, nullptr, nullptr, nullptr};
       void *ws = nullptr;
       float4 *dbox = nullptr;
-      if (prod_used) {  // data box for the shared-reciprocal guard
+      using AccT = typename AccSelNT<T, MODE, P2, EPS, Q>::type;
+      constexpr bool EXACT_FR = std::is_same<AccT, AccExactScr2<Q>>::value;
+      if (prod_used || EXACT_FR) {  // data box for the fast-path guards
         const int nb = (int)std::min<long long>(cdiv(L.n, 256), (long long)L.sms * 4);
         IDW_CK(cudaMallocAsync((void **)&dbox, sizeof(float4) * (nb + 1), L.st));
         k_bbox_partial<K, T><<<nb, 256, 0, L.st>>>(L.g, L.n, dbox + 1);
