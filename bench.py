@@ -65,6 +65,9 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
+    # test hooks for the multi-rank path on a single-GPU box (not used by the driver)
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl")
+    ap.add_argument("--device-override", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
@@ -218,13 +221,18 @@ def run_ours(args):
     world, rank, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    if args.device_override is not None:
+        local = args.device_override
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     n, m, layout, prec, variant, p, desc = CONFIGS[args.config]
     params = il.Params(p)

@@ -189,3 +189,31 @@ def test_fast_queries_on_data_points(il):
             assert np.array_equal(got, ref), (precision, s)
             assert np.array_equal(got, zs[idx]), (precision, s)
             assert st.fixup_queries == len(idx), (precision, s)
+
+
+def test_exact_zero_field_sign(il):
+    """z == 0 everywhere: the reference returns +0.0 (its sums start at +0);
+    the negated-sum EXACT path must not hand back -0.0."""
+    rng = np.random.default_rng(29)
+    data = random_records(rng, 1000)
+    data[:, 2] = 0.0
+    queries = random_queries(rng, 600)
+    for kind, precision in il.legal_pairs():
+        store = il.build(data, kind, precision)
+        ref = oracle.predict(store, queries)
+        for s in ("naive", "tiled"):
+            got = il.STRATEGIES[s](store, queries, cfg=il.ExecConfig(mode="exact"))
+            assert np.array_equal(got.view(np.uint8), ref.view(np.uint8)), (kind, precision, s)
+
+
+@pytest.mark.parametrize("kind", ["soa", "aos", "aoas"])
+def test_exact_tiled_bitwise_large(il, kind):
+    """fp32 EXACT tiled (packed IEEE + inline __frcp_rn fast path) against the
+    oracle's left-to-right loop, n = 65536 data x 4096 queries, bitwise."""
+    rng = np.random.default_rng(31)
+    data = random_records(rng, 65536)
+    queries = random_queries(rng, 4096)
+    store = il.build(data, il.LayoutKind(kind), il.Precision.single)
+    ref = oracle.predict(store, queries)
+    got = il.run_tiled(store, queries, cfg=il.ExecConfig(mode="exact"))
+    assert np.array_equal(got.view(np.uint8), ref.view(np.uint8))
