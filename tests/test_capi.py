@@ -1,0 +1,87 @@
+"""The C-ABI library: loads, exports every symbol include/idw_b200.h declares,
+and refuses to compute without a GPU (no CPU fallback).  CPU-only."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_1402_4986_b200 import _capi
+from paper_1402_4986_b200.layouts import LayoutKind, build
+from paper_1402_4986_b200.core import Precision
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "idw_b200.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(idw_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_abi():
+    fns = declared_functions()
+    assert {"idw_run", "idw_run_device", "idw_last_error", "idw_abi_version"} <= set(fns)
+    assert set(fns) == set(_capi.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(str(_capi.library_path()))
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_abi_version_and_struct_sizes():
+    lib = _capi.load()
+    assert lib.idw_abi_version() == _capi.ABI_VERSION == 1
+    # struct layouts of the header (x86-64): idw_store 72, idw_params 48, idw_stats 32
+    assert ctypes.sizeof(_capi.IdwStore) == 72
+    assert ctypes.sizeof(_capi.IdwParams) == 48
+    assert ctypes.sizeof(_capi.IdwStats) == 32
+
+
+def _store(kind=LayoutKind.SoA, precision=Precision.double):
+    rng = np.random.default_rng(0)
+    return build(rng.random((16, 3)), kind, precision)
+
+
+def test_structural_validation_without_gpu():
+    lib = _capi.load()
+    st = _store()
+    ns = _capi.make_store("soa", "double", st.count, [b.ctypes.data for b in st.buffers],
+                          [b.nbytes for b in st.buffers])
+    q = np.zeros(4)
+    out = np.zeros(4)
+    prm = _capi.make_params(2.0, 0.0, "tiled", "exact", 1024, 1024)
+    # illegal layout/precision pair is refused before any device work
+    bad = _capi.make_store("soaos", "single", st.count, [b.ctypes.data for b in st.buffers[:2]],
+                           [b.nbytes for b in st.buffers[:2]])
+    rc = lib.idw_run(ctypes.byref(bad), q.ctypes.data, q.ctypes.data, 4, ctypes.byref(prm), out.ctypes.data, None)
+    assert rc == -2 and b"double precision" in lib.idw_last_error()
+    # p <= 0
+    prm_bad = _capi.make_params(0.0, 0.0, "tiled", "exact", 1024, 1024)
+    rc = lib.idw_run(ctypes.byref(ns), q.ctypes.data, q.ctypes.data, 4, ctypes.byref(prm_bad), out.ctypes.data, None)
+    assert rc == -1 and b"power p" in lib.idw_last_error()
+    # buffer shorter than its shape
+    short = _capi.make_store("soa", "double", st.count, [b.ctypes.data for b in st.buffers], [8, 8, 8])
+    rc = lib.idw_run(ctypes.byref(short), q.ctypes.data, q.ctypes.data, 4, ctypes.byref(prm), out.ctypes.data, None)
+    assert rc == -1 and b"shorter" in lib.idw_last_error()
+
+
+@pytest.mark.skipif(_capi.device_count() > 0, reason="checks the no-GPU failure path")
+def test_no_cpu_fallback():
+    """Without a CUDA device every compute entry point fails loudly."""
+    st = _store()
+    ns = _capi.make_store("soa", "double", st.count, [b.ctypes.data for b in st.buffers],
+                          [b.nbytes for b in st.buffers])
+    q = np.full(4, 0.5)
+    out = np.zeros(4)
+    prm = _capi.make_params(2.0, 0.0, "naive", "exact", 1024, 1024)
+    with pytest.raises(_capi.NativeError, match="no CUDA device"):
+        _capi.run_host(ns, q, q, prm, out)
+    import paper_1402_4986_b200 as il
+
+    with pytest.raises(_capi.NativeError):
+        il.run_tiled(st, [(0.5, 0.5)])
