@@ -334,8 +334,8 @@ def run_ours(args):
         "kernel": "k_tiled" if variant == "tiled" else "k_nested",
         "kernel_ms": kmain,
         "fixup_ms": kfix,
-        "peak_source": "measured: idw_mufu_peak probe (rcp.approx chains on all SMs) in this run, "
-                       f"{probe_hz / 1e6:.0f} MHz implied; 16 MUFU lanes/clk/SM x {sms} SMs",
+        "peak_source": "measured: idw_mufu_peak probe (independent rcp.approx chains on all "
+                       f"{sms} SMs) just before the timed region; nominal 16 MUFU lanes/clk/SM",
         "peak_at_run_clock": run_clock_peak,
         "frac_at_run_clock": achieved / run_clock_peak if run_clock_peak else None,
         "algorithmic_unit": "one (query, data) pair = 1 rcp + 2 sums; n*m_shard pairs per launch",
@@ -411,7 +411,7 @@ def run_ours(args):
                        "l2": "flushed between steps (256 MiB write); inputs resident in HBM"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches[0],
-            "mufu_probe": {"rcp_per_s": probe_rate, "sm_mhz": probe_hz / 1e6},
+            "mufu_probe": {"rcp_per_s": probe_rate},
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

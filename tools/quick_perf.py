@@ -27,7 +27,7 @@ def run(n, m, kind, prec, variant, mode, p=2.0, reps=3, G=1024, splits=0):
     print(json.dumps(r), flush=True)
     return out
 
-if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "nested":
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "nested":  # noqa
     K = 1024
     run(1024 * K, 64 * K, "soa", "double", "nested_improved", "fast", p=3.5, reps=2)
     run(102400, 102400, "soa", "double", "nested_improved", "fast", p=2.0, reps=2)
