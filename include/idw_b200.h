@@ -130,6 +130,19 @@ int idw_run(const idw_store *store, const void *qx, const void *qy, int64_t m,
 int idw_run_device(const idw_store *store, const void *qx, const void *qy, int64_t m,
                    const idw_params *prm, void *out, void *stream, idw_stats *stats);
 
+/* Device-side layout packer: fp64 component arrays x, y, z (n device values
+ * each) cast round-to-nearest to the store's precision and written into the
+ * preallocated device buffers of `dst` in its layout, pads zeroed -- the
+ * bytes LayoutStore.from_arrays (layouts.py:172-186) produces.  Async on
+ * `stream`.                                                                */
+int idw_pack_device(const double *x, const double *y, const double *z, int64_t n,
+                    const idw_store *dst, int device, void *stream);
+
+/* Device-side layout converter: value copy from `src` to the preallocated
+ * `dst` (same precision and count, any legal kinds), byte-identical to
+ * LayoutStore.convert (layouts.py:251-255).  Async on `stream`.           */
+int idw_convert_device(const idw_store *src, const idw_store *dst, int device, void *stream);
+
 /* Device time of the last successful idw_run_device call on this thread:
  * the variant kernels (e.g. k_tiled [+ k_combine]) and the FAST fix-up pass,
  * from events recorded on the call's stream.  Blocks until they complete.   */

@@ -61,7 +61,8 @@ class IdwStats(ctypes.Structure):
 
 
 EXPORTS = ("idw_abi_version", "idw_device_count", "idw_last_error", "idw_run",
-           "idw_run_device", "idw_last_kernel_ms", "idw_mufu_peak")
+           "idw_run_device", "idw_pack_device", "idw_convert_device", "idw_last_kernel_ms",
+           "idw_mufu_peak")
 
 
 class NativeError(RuntimeError):
@@ -104,6 +105,10 @@ def load() -> ctypes.CDLL:
     lib.idw_run_device.restype = ctypes.c_int
     lib.idw_run_device.argtypes = [ctypes.POINTER(IdwStore), ptr, ptr, ctypes.c_int64,
                                    ctypes.POINTER(IdwParams), ptr, ptr, ctypes.POINTER(IdwStats)]
+    lib.idw_pack_device.restype = ctypes.c_int
+    lib.idw_pack_device.argtypes = [ptr, ptr, ptr, ctypes.c_int64, ctypes.POINTER(IdwStore), ctypes.c_int, ptr]
+    lib.idw_convert_device.restype = ctypes.c_int
+    lib.idw_convert_device.argtypes = [ctypes.POINTER(IdwStore), ctypes.POINTER(IdwStore), ctypes.c_int, ptr]
     lib.idw_last_kernel_ms.restype = ctypes.c_int
     lib.idw_last_kernel_ms.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
     lib.idw_mufu_peak.restype = ctypes.c_int
@@ -168,6 +173,15 @@ def run_device(store: IdwStore, qx_ptr: int, qy_ptr: int, m: int, params: IdwPar
     _check(lib.idw_run_device(ctypes.byref(store), qx_ptr, qy_ptr, m, ctypes.byref(params),
                               out_ptr, stream, ctypes.byref(stats)))
     return stats
+
+
+def pack_device(x_ptr: int, y_ptr: int, z_ptr: int, n: int, dst: IdwStore, device: int = 0,
+                stream: int = 0) -> None:
+    _check(load().idw_pack_device(x_ptr, y_ptr, z_ptr, n, ctypes.byref(dst), device, stream))
+
+
+def convert_device(src: IdwStore, dst: IdwStore, device: int = 0, stream: int = 0) -> None:
+    _check(load().idw_convert_device(ctypes.byref(src), ctypes.byref(dst), device, stream))
 
 
 def last_kernel_ms() -> tuple[float, float]:

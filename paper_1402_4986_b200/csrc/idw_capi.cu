@@ -281,6 +281,53 @@ int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const
   return rc;
 }
 
+// Shape check of a destination/source store against the layout table.
+static int check_store_shape(const idw_store *s, const char *what) {
+  if (!s) return set_error(std::string("null ") + what), IDW_E_ARG;
+  if (s->kind < 0 || s->kind > 4 || (s->precision != IDW_SINGLE && s->precision != IDW_DOUBLE))
+    return set_error(std::string(what) + ": unknown layout or precision"), IDW_E_ARG;
+  if (s->precision == IDW_SINGLE && (s->kind == IDW_SOAOS || s->kind == IDW_HYBRID))
+    return set_error("layout requires double precision"), IDW_E_UNSUPPORTED;
+  if (s->count < 1) return set_error("no data points"), IDW_E_ARG;
+  if (s->nbuf != nbuf_of(s->kind)) return set_error(std::string(what) + ": buffer count does not match layout"), IDW_E_ARG;
+  for (int b = 0; b < s->nbuf; ++b) {
+    if (!s->buf[b]) return set_error(std::string(what) + ": null buffer"), IDW_E_ARG;
+    if (s->nbytes[b] < s->count * (int64_t)bytes_per_point(s->kind, s->precision, b))
+      return set_error(std::string(what) + ": buffer shorter than its shape"), IDW_E_ARG;
+  }
+  return 0;
+}
+
+int idw_pack_device(const double *x, const double *y, const double *z, int64_t n, const idw_store *dst,
+                    int device, void *stream) {
+  g_err.clear();
+  int rc = check_store_shape(dst, "destination");
+  if (rc) return rc;
+  if (!x || !y || !z) return set_error("null component array"), IDW_E_ARG;
+  if (n != dst->count) return set_error("component length != store count"), IDW_E_ARG;
+  cudaStream_t st;
+  int sms;
+  if ((rc = device_stream(device, &st, &sms))) return rc;
+  unsigned char *d[3] = {(unsigned char *)dst->buf[0], (unsigned char *)dst->buf[1], (unsigned char *)dst->buf[2]};
+  return pack_device(x, y, z, n, dst->kind, dst->precision, d, (cudaStream_t)stream, sms);
+}
+
+int idw_convert_device(const idw_store *src, const idw_store *dst, int device, void *stream) {
+  g_err.clear();
+  int rc = check_store_shape(src, "source");
+  if (rc) return rc;
+  if ((rc = check_store_shape(dst, "destination"))) return rc;
+  if (src->precision != dst->precision) return set_error("conversion keeps the precision"), IDW_E_ARG;
+  if (src->count != dst->count) return set_error("source and destination counts differ"), IDW_E_ARG;
+  cudaStream_t st;
+  int sms;
+  if ((rc = device_stream(device, &st, &sms))) return rc;
+  const unsigned char *s3[3] = {(const unsigned char *)src->buf[0], (const unsigned char *)src->buf[1],
+                                (const unsigned char *)src->buf[2]};
+  unsigned char *d3[3] = {(unsigned char *)dst->buf[0], (unsigned char *)dst->buf[1], (unsigned char *)dst->buf[2]};
+  return convert_device(s3, src->kind, d3, dst->kind, src->precision, src->count, (cudaStream_t)stream, sms);
+}
+
 int idw_last_kernel_ms(double *variant_ms, double *fixup_ms) {
   g_err.clear();
   if (g_last_dev < 0) return set_error("no completed idw_run_device call on this thread"), IDW_E_ARG;

@@ -107,6 +107,12 @@ int launch_nested(Launch &L);
 int launch_nested_orig(Launch &L);
 int launch_fixup(Launch &L);
 
+// Device-side layout packers/converters (idw_layout_dev.cu).
+int pack_device(const double *x, const double *y, const double *z, long long n, int kind, int prec,
+                unsigned char *const *dst, cudaStream_t st, int sms);
+int convert_device(const unsigned char *const *src, int kin, unsigned char *const *dst, int kout, int prec,
+                   long long n, cudaStream_t st, int sms);
+
 // Does this launch write screen flags and need the fix-up pass?
 inline bool needs_fixup(const Launch &L) {
   if (L.variant == IDW_NESTED_ORIGINAL) return false;

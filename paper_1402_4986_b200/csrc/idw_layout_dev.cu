@@ -1,0 +1,129 @@
+// Device-side layout packers and converters (the "layout packers/converters"
+// subsystem of the north star), byte-identical to the reference's host code:
+//   k_pack     <- LayoutStore.from_arrays  (layouts.py:172-186): fp64 x, y, z
+//                 cast round-to-nearest to the run dtype (numpy astype) and
+//                 written in the shape table's strides; pads written as zero
+//   k_convert  <- LayoutStore.convert      (layouts.py:251-255): value copy
+//                 between two layouts of the same precision
+// One thread per point (grid-stride); each kernel is a single HBM pass.
+#include <algorithm>
+
+#include "idw_kernels.cuh"
+#include "idw_launch.h"
+
+namespace idw {
+
+struct WBufs {
+  unsigned char *b[3];
+};
+
+template <int K, typename T>
+struct GStore;
+template <typename T>
+struct GStore<SOA, T> {
+  static __device__ __forceinline__ void put(const WBufs &w, long long i, T x, T y, T z) {
+    reinterpret_cast<T *>(w.b[0])[i] = x;
+    reinterpret_cast<T *>(w.b[1])[i] = y;
+    reinterpret_cast<T *>(w.b[2])[i] = z;
+  }
+};
+template <typename T>
+struct GStore<AOS, T> {
+  static __device__ __forceinline__ void put(const WBufs &w, long long i, T x, T y, T z) {
+    T *r = reinterpret_cast<T *>(w.b[0]) + 3 * i;
+    r[0] = x;
+    r[1] = y;
+    r[2] = z;
+  }
+};
+template <>
+struct GStore<AOAS, float> {
+  static __device__ __forceinline__ void put(const WBufs &w, long long i, float x, float y, float z) {
+    reinterpret_cast<float4 *>(w.b[0])[i] = make_float4(x, y, z, 0.f);
+  }
+};
+template <>
+struct GStore<AOAS, double> {
+  static __device__ __forceinline__ void put(const WBufs &w, long long i, double x, double y, double z) {
+    double2 *r = reinterpret_cast<double2 *>(w.b[0]) + 2 * i;
+    r[0] = make_double2(x, y);
+    r[1] = make_double2(z, 0.0);
+  }
+};
+template <>
+struct GStore<SOAOS, double> {
+  static __device__ __forceinline__ void put(const WBufs &w, long long i, double x, double y, double z) {
+    reinterpret_cast<double2 *>(w.b[0])[i] = make_double2(x, y);
+    reinterpret_cast<double2 *>(w.b[1])[i] = make_double2(z, 0.0);
+  }
+};
+template <>
+struct GStore<HYBRID, double> {
+  static __device__ __forceinline__ void put(const WBufs &w, long long i, double x, double y, double z) {
+    reinterpret_cast<double2 *>(w.b[0])[i] = make_double2(x, y);
+    reinterpret_cast<double *>(w.b[1])[i] = z;
+  }
+};
+
+template <int K, typename T>
+__global__ void __launch_bounds__(256) k_pack(const double *__restrict__ x, const double *__restrict__ y,
+                                              const double *__restrict__ z, long long n, WBufs w) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    GStore<K, T>::put(w, i, (T)x[i], (T)y[i], (T)z[i]);  // (float)double is RN == numpy astype
+}
+
+template <int KI, int KO, typename T>
+__global__ void __launch_bounds__(256) k_convert(Bufs in, long long n, WBufs w) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    T x, y, z;
+    GFetch<KI, T>::get(in, i, x, y, z);
+    GStore<KO, T>::put(w, i, x, y, z);
+  }
+}
+
+static int grid_for(long long n, int sms) {
+  return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, (long long)sms * 16));
+}
+
+// Visit the legal (layout, dtype) of a (kind, prec) pair.
+template <class F>
+static int visit_kind(int kind, int prec, F &&f) {
+  Launch L;
+  L.kind = kind;
+  L.prec = prec;
+  return with_layout(L, std::forward<F>(f));
+}
+
+int pack_device(const double *x, const double *y, const double *z, long long n, int kind, int prec,
+                unsigned char *const *dst, cudaStream_t st, int sms) {
+  WBufs w{{dst[0], dst[1], dst[2]}};
+  return visit_kind(kind, prec, [&](auto KC, auto tv) -> int {
+    using T = decltype(tv);
+    constexpr int K = decltype(KC)::value;
+    k_pack<K, T><<<grid_for(n, sms), 256, 0, st>>>(x, y, z, n, w);
+    IDW_CK_LAUNCH();
+    return 0;
+  });
+}
+
+int convert_device(const unsigned char *const *src, int kin, unsigned char *const *dst, int kout, int prec,
+                   long long n, cudaStream_t st, int sms) {
+  Bufs in{{src[0], src[1], src[2]}};
+  WBufs w{{dst[0], dst[1], dst[2]}};
+  return visit_kind(kin, prec, [&](auto KIC, auto tv) -> int {
+    using T = decltype(tv);
+    constexpr int KI = decltype(KIC)::value;
+    return visit_kind(kout, prec, [&](auto KOC, auto tv2) -> int {
+      constexpr int KO = decltype(KOC)::value;
+      if constexpr (std::is_same<T, decltype(tv2)>::value) {
+        k_convert<KI, KO, T><<<grid_for(n, sms), 256, 0, st>>>(in, n, w);
+        IDW_CK_LAUNCH();
+        return 0;
+      } else {
+        return (int)IDW_E_UNSUPPORTED;
+      }
+    });
+  });
+}
+
+}  // namespace idw

@@ -50,6 +50,96 @@ class DeviceStore:
         self.nbytes = list(nbytes)
         return self
 
+    # -- device-side packers / converters / dump loader (§8f rows) -----------
+    @classmethod
+    def _alloc(cls, kind, precision, count, device, stats=None):
+        import torch
+
+        from .layouts import AccessStats, buffer_shapes
+
+        shapes = buffer_shapes(kind, precision, count)
+        dev = torch.device("cuda", device)
+        tensors = [torch.zeros(sh.nbytes + PAD, dtype=torch.uint8, device=dev) for sh in shapes]
+        self = cls.from_tensors(kind, precision, count, tensors, [sh.nbytes for sh in shapes], device,
+                                stats or AccessStats(precision.itemsize))
+        self.shapes = shapes
+        return self
+
+    @classmethod
+    def from_arrays(cls, x, y, z, kind, precision, device: int = 0):
+        """Pack fp64 component arrays on the GPU (idw_pack_device): the same
+        bytes as LayoutStore.from_arrays (reference layouts.py:172-186)."""
+        import torch
+
+        from .layouts import check_legal
+
+        check_legal(kind, precision)
+        dev = torch.device("cuda", device)
+        comps = [torch.as_tensor(np.asarray(a, dtype=np.float64)).to(dev) for a in (x, y, z)]
+        n = int(comps[0].numel())
+        if n == 0:
+            raise ValueError("no data points")
+        self = cls._alloc(kind, precision, n, device)
+        _capi.pack_device(comps[0].data_ptr(), comps[1].data_ptr(), comps[2].data_ptr(), n, self.native(), device,
+                          torch.cuda.current_stream(dev).cuda_stream)
+        return self
+
+    def convert(self, target):
+        """Re-layout on the GPU (idw_convert_device), value-preserving like
+        LayoutStore.convert (reference layouts.py:251-255)."""
+        import torch
+
+        from .layouts import check_legal
+
+        check_legal(target, self.precision)
+        out = DeviceStore._alloc(target, self.precision, self.count, self.device)
+        _capi.convert_device(self.native(), out.native(), self.device,
+                             torch.cuda.current_stream(self.device).cuda_stream)
+        return out
+
+    def to_host(self):
+        """Copy the raw buffers back into a host LayoutStore (byte-exact)."""
+        from .layouts import LayoutStore, aligned_zeros, buffer_shapes
+
+        shapes = buffer_shapes(self.kind, self.precision, self.count)
+        bufs = []
+        for t, sh in zip(self.tensors, shapes):
+            b = aligned_zeros(sh.nbytes)
+            b[:] = t[: sh.nbytes].cpu().numpy()
+            bufs.append(b)
+        return LayoutStore(self.kind, self.precision, self.count, bufs, shapes)
+
+    @classmethod
+    def from_dump(cls, path, device: int = 0):
+        """Load an IDWL dump (reference layouts.py:257-294: <4sBBQ> header +
+        raw buffers) straight into device buffers, skipping the host repack."""
+        import torch
+
+        from .layouts import DUMP_HEADER, DUMP_MAGIC, KIND_CODE, PRECISION_CODE, buffer_shapes
+
+        with open(path, "rb") as fh:
+            blob = fh.read()
+        if len(blob) < DUMP_HEADER.size:
+            raise ValueError("truncated layout dump")
+        magic, kcode, pcode, count = DUMP_HEADER.unpack_from(blob)
+        if magic != DUMP_MAGIC:
+            raise ValueError("bad magic; not a layout dump")
+        kinds = {v: k for k, v in KIND_CODE.items()}
+        precs = {v: k for k, v in PRECISION_CODE.items()}
+        if kcode not in kinds or pcode not in precs:
+            raise ValueError("unknown layout or precision code")
+        kind, precision = kinds[kcode], precs[pcode]
+        shapes = buffer_shapes(kind, precision, count)
+        if len(blob) != DUMP_HEADER.size + sum(sh.nbytes for sh in shapes):
+            raise ValueError("layout dump has wrong size")
+        self = cls._alloc(kind, precision, count, device)
+        pos = DUMP_HEADER.size
+        for t, sh in zip(self.tensors, shapes):
+            host = torch.frombuffer(bytearray(blob[pos:pos + sh.nbytes]), dtype=torch.uint8)
+            t[: sh.nbytes].copy_(host)
+            pos += sh.nbytes
+        return self
+
     @property
     def dtype(self):
         import torch

@@ -217,3 +217,25 @@ def test_exact_tiled_bitwise_large(il, kind):
     ref = oracle.predict(store, queries)
     got = il.run_tiled(store, queries, cfg=il.ExecConfig(mode="exact"))
     assert np.array_equal(got.view(np.uint8), ref.view(np.uint8))
+
+
+def test_device_packers_converters_and_dump_loader(il, tmp_path):
+    """idw_pack_device / idw_convert_device / DeviceStore.from_dump produce the
+    reference's bytes (host LayoutStore as the byte oracle, itself pinned to
+    the reference's dumps in test_host.py)."""
+    from paper_1402_4986_b200.device import DeviceStore
+
+    rng = np.random.default_rng(37)
+    recs = rng.random((1001, 3)) * np.array([1.0, 1.0, 100.0])
+    for precision in il.Precision:
+        kinds = [k for k in il.LayoutKind if k.legal_for(precision)]
+        for a in kinds:
+            host = il.build(recs, a, precision)
+            dev = DeviceStore.from_arrays(recs[:, 0], recs[:, 1], recs[:, 2], a, precision)
+            assert dev.to_host().to_bytes() == host.to_bytes(), (a, precision)
+            for b in kinds:
+                conv = dev.convert(b).to_host()
+                assert conv.to_bytes() == host.convert(b).to_bytes(), (a, b, precision)
+            path = tmp_path / f"{a.value}_{precision.value}.idwl"
+            host.dump(path)
+            assert DeviceStore.from_dump(path).to_host().to_bytes() == host.to_bytes()
