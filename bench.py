@@ -342,6 +342,22 @@ def run_ours(args):
     }
     if prec == "double":
         roof["note"] = "fp64 kernels are FP64-pipe bound; the MUFU figure is only a reference line"
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture
+    prof = ROOT / "profiles" / "r1" / f"prof_{args.config}_tiled.raw.csv"
+    if prof.exists() and args.mode == "fast":
+        import csv
+
+        rows = list(csv.reader(open(prof)))
+        d = dict(zip(rows[0], rows[2]))
+        u = dict(zip(rows[0], rows[1]))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        try:
+            tb = sum(float(d[k]) * scale[u[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            roof["traffic"] = tb
+            roof["traffic_source"] = f"{prof.relative_to(ROOT)} (ncu --set full, one launch, same config)"
+            roof["algorithmic_bytes"] = float(n * (16 if layout == "aoas" else 12) + 2 * (hi - lo) * 4)
+        except (KeyError, ValueError):
+            pass
 
     # ---- e2e through the public drop-in API (host buffers, blocking)
     e2e = None
