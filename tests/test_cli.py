@@ -39,7 +39,7 @@ def test_cli_run_matches_oracle(tmp_path):
     qs = rng.random((64, 2))
     cli.write_points_csv(tmp_path / "d.csv", recs)
     with open(tmp_path / "q.csv", "w") as fh:
-        fh.write("x,y\n" + "".join(f"{a!r},{b!r}\n" for a, b in qs))
+        fh.write("x,y\n" + "".join(f"{float(a)!r},{float(b)!r}\n" for a, b in qs))
     for strategy in ("seq", "naive", "tiled", "nested-improved", "nested-original"):
         out = tmp_path / f"{strategy}.csv"
         assert cli.main(["run", "--data", str(tmp_path / "d.csv"), "--queries", str(tmp_path / "q.csv"),
