@@ -1,6 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -q -m gpu --timeout 600 -x > gpurun_out/pytest_gpu.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 600 python tools/quick_perf.py nested > gpurun_out/quick_perf_nested.log 2>&1
 timeout 600 python tools/quick_perf.py > gpurun_out/quick_perf.log 2>&1
+bash tools/gpu_xcheck.sh
