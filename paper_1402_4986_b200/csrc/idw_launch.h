@@ -117,7 +117,7 @@ int convert_device(const unsigned char *const *src, int kin, unsigned char *cons
 inline bool needs_fixup(const Launch &L) {
   if (L.variant == IDW_NESTED_ORIGINAL) return false;
   if (L.mode == FAST) return true;
-  return !L.epsp && (L.variant == IDW_NAIVE || L.variant == IDW_TILED);  // screened EXACT
+  return !L.epsp && L.variant != IDW_NESTED_ORIGINAL;  // screened EXACT
 }
 
 }  // namespace idw
