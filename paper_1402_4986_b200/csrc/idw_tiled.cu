@@ -46,8 +46,16 @@ struct Shape {
   long long qpc, blocks, splits, tps;
 };
 static Shape shape_grid(long long m, long long ntiles, long long slots, int Q, int nc_max, bool allow_split,
-                        int forced_splits) {
+                        int forced_splits, long long sms) {
   const long long cap = (long long)nc_max * Q;
+  if (!allow_split && cdiv(m, cap) < sms) {
+    // EXACT (no data splits): spread few queries over every SM, one block
+    // each, rather than fill fewer SMs with full blocks (measured: C2 exact
+    // ran 100 full blocks on 148 SMs).
+    const long long blocks = std::max<long long>(1, std::min<long long>(sms, cdiv(m, (long long)Q * 32)));
+    const long long qpc = cdiv(cdiv(m, blocks), Q) * Q;
+    return {qpc, cdiv(m, qpc), 1, ntiles};
+  }
   const long long min_q = std::min<long long>(cap / 2, cdiv(m, Q) * Q);
   Shape best{0, 0, 0, 0};
   double best_cost = 0;
@@ -106,7 +114,7 @@ int launch_tiled(Launch &L) {
       if (occ < 1) occ = 1;
       const long long slots = (long long)L.sms * occ;
       const long long ntiles = cdiv(L.n, TILE);
-      const Shape sh = shape_grid(L.m, ntiles, slots, Q, C::NC_MAX, MODE == FAST, L.splits);
+      const Shape sh = shape_grid(L.m, ntiles, slots, Q, C::NC_MAX, MODE == FAST, L.splits, L.sms);
       const int nc = (int)cdiv(cdiv(sh.qpc, Q), 32) * 32;
       const int smem = (nc / 32) * RING;
 
