@@ -33,6 +33,12 @@ if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "nested":  # 
     run(102400, 102400, "soa", "double", "nested_improved", "fast", p=2.0, reps=2)
     run(10240 * K, 100 * K, "aoas", "single", "nested_improved", "fast", reps=2)
     sys.exit(0)
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "exact":  # noqa
+    K = 1024
+    for v in ("naive", "tiled", "nested_improved", "nested_original"):
+        for prec, kind in (("single", "aoas"), ("double", "soa")):
+            run(100 * K, 100 * K if v != "nested_original" else 8 * K, kind, prec, v, "exact", reps=2)
+    sys.exit(0)
 if __name__ == "__main__":
     rate, hz = il._capi.mufu_peak(0)
     print(json.dumps(dict(mufu_rcp_per_s=rate, pairs_roofline_gpairs=rate / 1e9, sm_hz=hz)), flush=True)
