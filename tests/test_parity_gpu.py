@@ -239,3 +239,51 @@ def test_device_packers_converters_and_dump_loader(il, tmp_path):
             path = tmp_path / f"{a.value}_{precision.value}.idwl"
             host.dump(path)
             assert DeviceStore.from_dump(path).to_host().to_bytes() == host.to_bytes()
+
+
+def test_single_query_large_n_all_variants(il):
+    """m = 1 against n = 300000 (FAST splits the data across the whole GPU;
+    EXACT runs one block): exact bitwise vs oracle, fast within tolerance."""
+    rng = np.random.default_rng(43)
+    data = random_records(rng, 300_000, -50.0, 50.0)
+    q = random_queries(rng, 1)
+    for precision in il.Precision:
+        store = il.build(data, il.LayoutKind.SoA, precision)
+        ref = oracle.predict(store, q)
+        truth = oracle.truth(store, q)
+        for s in ("naive", "tiled"):
+            assert np.array_equal(il.STRATEGIES[s](store, q, cfg=il.ExecConfig(mode="exact")), ref), (precision, s)
+            assert rel(il.STRATEGIES[s](store, q, cfg=il.ExecConfig(mode="fast")), truth) <= TOL[precision.value]
+        got = il.run_nested_improved(store, q, cfg=il.ExecConfig(mode="exact"))
+        assert np.array_equal(got, oracle.nested_improved(store, q)), precision
+
+
+def test_translation_invariance_exact(il):
+    """Dyadic-grid coordinates shifted by integers give bit-identical results
+    (reference test_core.py:137-163), through the GPU EXACT path."""
+    rng = np.random.default_rng(47)
+    data = random_records(rng, 2000)
+    data[:, :2] = np.round(data[:, :2] * 2 ** 10) / 2 ** 10
+    queries = np.round(random_queries(rng, 300) * 2 ** 10) / 2 ** 10
+    for precision in il.Precision:
+        base = il.run_tiled(il.build(data, il.LayoutKind.AoS, precision), queries, cfg=il.ExecConfig(mode="exact"))
+        moved = data.copy()
+        moved[:, 0] += 33.0
+        moved[:, 1] -= 150.0
+        got = il.run_tiled(il.build(moved, il.LayoutKind.AoS, precision), queries + np.array([33.0, -150.0]),
+                           cfg=il.ExecConfig(mode="exact"))
+        assert np.array_equal(got, base), precision
+
+
+def test_negative_values_and_hull(il):
+    """Negative z and coordinates; predictions stay inside the value hull
+    (reference test_core.py:165-173)."""
+    rng = np.random.default_rng(53)
+    data = random_records(rng, 5000, -3.0, 7.0)
+    data[:, :2] -= 0.5
+    queries = random_queries(rng, 2000) - 0.5
+    for mode in ("exact", "fast"):
+        for kind, precision in il.legal_pairs():
+            got = il.run_tiled(il.build(data, kind, precision), queries, cfg=il.ExecConfig(mode=mode))
+            slack = 1e-4 if precision is il.Precision.single else 1e-12
+            assert got.min() >= -3.0 - slack and got.max() <= 7.0 + slack, (mode, kind, precision)
