@@ -27,6 +27,9 @@ def run(n, m, kind, prec, variant, mode, p=2.0, reps=3, G=1024, splits=0):
     print(json.dumps(r), flush=True)
     return out
 
+import subprocess as _sp
+print(json.dumps({"clocks": _sp.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                                     "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()}), flush=True)
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "nested":  # noqa
     K = 1024
     run(1024 * K, 64 * K, "soa", "double", "nested_improved", "fast", p=3.5, reps=2)
@@ -37,7 +40,7 @@ if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "exact":  # n
     K = 1024
     for v in ("naive", "tiled", "nested_improved", "nested_original"):
         for prec, kind in (("single", "aoas"), ("double", "soa")):
-            run(100 * K, 100 * K if v != "nested_original" else 8 * K, kind, prec, v, "exact", reps=2)
+            run(100 * K, 100 * K if v != "nested_original" else 8 * K, kind, prec, v, "exact", reps=5)
     sys.exit(0)
 if __name__ == "__main__":
     rate, hz = il._capi.mufu_peak(0)
