@@ -287,3 +287,33 @@ def test_negative_values_and_hull(il):
             got = il.run_tiled(il.build(data, kind, precision), queries, cfg=il.ExecConfig(mode=mode))
             slack = 1e-4 if precision is il.Precision.single else 1e-12
             assert got.min() >= -3.0 - slack and got.max() <= 7.0 + slack, (mode, kind, precision)
+
+
+def test_device_resident_path_matches_host_path(il):
+    """predict_device (the bench/serving path: HBM-resident store, async on
+    the torch stream) == the blocking host API, bitwise, every variant/mode;
+    plus the kernel-time and MUFU-probe entry points."""
+    import torch
+
+    from paper_1402_4986_b200 import _capi
+    from paper_1402_4986_b200.device import DeviceStore, predict_device
+
+    rng = np.random.default_rng(59)
+    data = random_records(rng, 20000)
+    queries = random_queries(rng, 3000)
+    for kind, precision in (("aoas", il.Precision.single), ("soa", il.Precision.double)):
+        store = il.build(data, il.LayoutKind(kind), precision)
+        ds = DeviceStore(store, 0)
+        dt = ds.dtype
+        q = [torch.tensor(queries[:, k].astype(precision.dtype), device="cuda") for k in (0, 1)]
+        for variant in ("naive", "tiled", "nested_improved", "nested_original"):
+            for mode in ("exact", "fast"):
+                cfg = il.ExecConfig(mode=mode, group_size=256)
+                host = il.STRATEGIES[variant](store, queries, cfg=cfg)
+                out = torch.empty(len(queries), dtype=dt, device="cuda")
+                predict_device(ds, q[0], q[1], out, il.Params(), cfg, variant)
+                ms, fix_ms = _capi.last_kernel_ms()
+                assert ms > 0 and fix_ms >= 0
+                assert np.array_equal(out.cpu().numpy(), host), (kind, variant, mode)
+    rate, _ = _capi.mufu_peak(0)
+    assert 1e12 < rate < 2e13  # ~148 SMs x 16/clk x ~2 GHz
