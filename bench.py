@@ -324,12 +324,21 @@ def run_ours(args):
     run_clock_peak = None
     if clocks.get("sm_mhz"):
         run_clock_peak = sms * 16 * clocks["sm_mhz"] * 1e6 / mufu_per_pair / 1e9
+    peak = probe_rate / mufu_per_pair / 1e9
+    if prec == "double":
+        # FP64-pipe bound: DP ops per pair of the FAST fp64 loop (SASS):
+        # p = 2: 2 DADD + DMUL + DFMA (d2) + 3 DFMA (rcp correction) + DADD + DFMA = 9;
+        # p = 3.5 / 3: 6 base + 6 (quarter-root cubic step) + 4 / 3 (power) = 16 / 15
+        dp_ops = {2.0: 9, 3.5: 16, 3.0: 15}.get(p, 50)
+        mhz = clocks.get("sm_mhz") or 1965.0
+        peak = sms * 64 * mhz * 1e6 / dp_ops / 1e9  # nominal 64 DP lanes/clk/SM (62 measured)
+        run_clock_peak = peak
     roof = {
         "bound": "mufu" if prec == "single" else "fp64",
         "achieved": achieved,
-        "peak": probe_rate / mufu_per_pair / 1e9,
+        "peak": peak,
         "unit": "GPairs/s",
-        "frac": achieved / (probe_rate / mufu_per_pair / 1e9),
+        "frac": achieved / peak,
         "traffic": None,
         "kernel": "k_tiled" if variant == "tiled" else "k_nested",
         "kernel_ms": kmain,
@@ -341,7 +350,8 @@ def run_ours(args):
         "algorithmic_unit": "one (query, data) pair = 1 rcp + 2 sums; n*m_shard pairs per launch",
     }
     if prec == "double":
-        roof["note"] = "fp64 kernels are FP64-pipe bound; the MUFU figure is only a reference line"
+        roof["peak_source"] = (f"FP64 pipe: {sms} SMs x 64 DP lanes/clk x run clock / {dp_ops} DP ops per pair "
+                               "(DFMA measured 62/clk/SM in tools/microbench.cu)")
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
     prof = ROOT / "profiles" / "r1" / f"prof_{args.config}_tiled.raw.csv"
     if prof.exists() and args.mode == "fast":
