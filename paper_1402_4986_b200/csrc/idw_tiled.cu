@@ -65,7 +65,9 @@ static Shape shape_grid(long long m, long long ntiles, long long slots, int Q, i
       if (qpc < min_q) break;   // more waves only shrink blocks further
       blocks = cdiv(m, qpc);
       const long long waves = cdiv(blocks * splits, slots);
-      const double cost = (double)waves * (double)qpc * (double)tps;
+      // a CTA runs whole warps: charge the query slots its warps hold
+      const long long qslots = cdiv(qpc, (long long)Q * 32) * Q * 32;
+      const double cost = (double)waves * (double)qslots * (double)tps;
       if (best.qpc == 0 || cost < best_cost * 0.999) {
         best = {qpc, blocks, splits, tps};
         best_cost = cost;
