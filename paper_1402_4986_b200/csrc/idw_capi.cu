@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -101,6 +102,17 @@ static int device_stream(int dev, cudaStream_t *st, int *sms) {
   if (!g_streams[dev]) {
     IDW_CK(cudaStreamCreateWithFlags(&g_streams[dev], cudaStreamNonBlocking));
     IDW_CK(cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev));
+    // Per-call scratch (flags, split partials, data box) comes from the
+    // device's default stream-ordered pool.  With the default release
+    // threshold (0) every synchronisation hands the pages back and the next
+    // call re-maps them (measured ~ms per call at C1); keep them instead.
+    const char *keep = getenv("IDW_POOL_KEEP");
+    if (!keep || atoi(keep) != 0) {
+      cudaMemPool_t pool;
+      IDW_CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+      uint64_t thr = ~uint64_t(0);
+      IDW_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
   }
   *st = g_streams[dev];
   *sms = g_sms[dev];

@@ -103,6 +103,12 @@ int launch_tiled(Launch &L) {
         if (prod == 2) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 2>;
         prod_used = prod == 1 || prod == 2;
       }
+      if constexpr (sizeof(T) == 8 && MODE == FAST && !P2) {
+        // compile-time powers for the common half-integer p (p = 3: jq 6, p = 3.5: jq 7)
+        const int jq = make_scal<T>(L).jq;
+        if (jq == 7) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 0, 7>;
+        if (jq == 6) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 0, 6>;
+      }
       const int smem_max = (C::NC_MAX / 32) * RING;
       IDW_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
       int occ = 0;

@@ -317,3 +317,25 @@ def test_device_resident_path_matches_host_path(il):
                 assert np.array_equal(out.cpu().numpy(), host), (kind, variant, mode)
     rate, _ = _capi.mufu_peak(0)
     assert 1e12 < rate < 2e13  # ~148 SMs x 16/clk x ~2 GHz
+
+
+@pytest.mark.parametrize("scale", [1e-70, 1e-20, 1e-3, 1.0, 1e18, 1e40])
+def test_fast_fp64_general_p_scales(il, scale):
+    """FAST fp64 general p (quarter-root series for p in multiples of 1/2,
+    exp2/log2 otherwise) across coordinate scales that put d2 below 2^-125 or
+    above 2^125 -- outside the fp32 seed range every such weight is forced to
+    NaN, so the query must come back through the exact fix-up -- and a few
+    near-coincident queries.  Within 1e-12 of the fp64 truth, finite."""
+    rng = np.random.default_rng(61)
+    data = random_records(rng, 6000)
+    data[:, :2] *= scale
+    queries = random_queries(rng, 1500) * scale
+    queries[:5] = data[:5, :2] * (1.0 + 1e-9)  # near-coincident (tiny d2 only)
+    for kind in (il.LayoutKind.SoA, il.LayoutKind.AoaS):
+        store = il.build(data, kind, il.Precision.double)
+        for p in (3.5, 3.0, 1.5, 2.7):
+            truth = oracle.truth(store, queries, p)
+            for s in ("tiled", "naive", "nested_improved"):
+                got = il.STRATEGIES[s](store, queries, il.Params(p), cfg=il.ExecConfig(mode="fast"))
+                assert np.all(np.isfinite(got)), (scale, kind, p, s)
+                assert rel(got, truth) <= 1e-12, (scale, kind, p, s)
