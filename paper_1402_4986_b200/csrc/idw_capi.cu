@@ -9,7 +9,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 
 #include "idw_launch.h"
@@ -86,6 +88,31 @@ static int validate(const idw_store *s, const void *qx, const void *qy, int64_t 
 }
 
 static std::mutex g_mu;
+
+int kernel_occupancy(const void *kern, int dev, int threads, int smem, int *occ) {
+  struct Key {
+    const void *k;
+    int dev, threads, smem;
+    bool operator<(const Key &o) const {
+      return std::tie(k, dev, threads, smem) < std::tie(o.k, o.dev, o.threads, o.smem);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, int> cache;
+  const Key key{kern, dev, threads, smem};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return *occ = it->second, 0;
+  }
+  if (smem > 48 * 1024) IDW_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int o = 0;
+  IDW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem));
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = o;
+  *occ = o;
+  return 0;
+}
 static cudaStream_t g_streams[64];
 static int g_sms[64];
 

@@ -100,6 +100,11 @@ inline Scal<T> make_scal(const Launch &L) {
   return s;
 }
 
+// cudaFuncSetAttribute(max dynamic smem) + resident CTAs per SM for `kern`
+// at (threads, smem), done once per (kernel, device) and cached: both calls
+// cost host microseconds that small launches cannot hide.
+int kernel_occupancy(const void *kern, int dev, int threads, int smem, int *occ);
+
 // Per-variant launchers (one translation unit each).
 int launch_naive(Launch &L);
 int launch_tiled(Launch &L);

@@ -110,9 +110,8 @@ int launch_tiled(Launch &L) {
         if (jq == 6) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 0, 6>;
       }
       const int smem_max = (C::NC_MAX / 32) * RING;
-      IDW_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
       int occ = 0;
-      IDW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NC_MAX, smem_max));
+      if (int rc = kernel_occupancy((const void *)kern, L.dev, C::NC_MAX, smem_max, &occ)) return rc;
       if (occ < 1) occ = 1;
       const long long slots = (long long)L.sms * occ;
       const long long ntiles = cdiv(L.n, TILE);
@@ -124,7 +123,8 @@ int launch_tiled(Launch &L) {
       void *ws = nullptr;
       float4 *dbox = nullptr;
       using AccT = typename AccSelNT<T, MODE, P2, EPS, Q>::type;
-      constexpr bool EXACT_FR = std::is_same<AccT, AccExactScr2<Q>>::value;
+      constexpr bool EXACT_FR = std::is_same<AccT, AccExactScr2<Q>>::value ||
+                               std::is_same<AccT, AccExactScr<double, true, Q>>::value;
       if (prod_used || EXACT_FR) {  // data box for the fast-path guards
         const int nb = (int)std::min<long long>(cdiv(L.n, 256), (long long)L.sms * 4);
         IDW_CK(cudaMallocAsync((void **)&dbox, sizeof(float4) * (nb + 1), L.st));

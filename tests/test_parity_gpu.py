@@ -339,3 +339,24 @@ def test_fast_fp64_general_p_scales(il, scale):
                 got = il.STRATEGIES[s](store, queries, il.Params(p), cfg=il.ExecConfig(mode="fast"))
                 assert np.all(np.isfinite(got)), (scale, kind, p, s)
                 assert rel(got, truth) <= 1e-12, (scale, kind, p, s)
+
+
+@pytest.mark.parametrize("scale", [1e-160, 1e-140, 1e-3, 1e150])
+def test_exact_fp64_scales_bitwise(il, scale):
+    """fp64 EXACT p = 2 across exponent ranges: d2 ~ 1e-320 (denormal: the
+    inline __drcp_rn path seeds inf, the query is screened and recomputed),
+    d2 ~ 1e-280 (inline path, normal range), d2 ~ 1e300 (box guard off: the
+    library __drcp_rn).  Bitwise against the reference loop (NaN where the
+    reference itself overflows to inf/inf)."""
+    rng = np.random.default_rng(67)
+    data = random_records(rng, 3000)
+    data[:, :2] *= scale
+    queries = random_queries(rng, 700) * scale
+    for kind in (il.LayoutKind.SoA, il.LayoutKind.AoaS, il.LayoutKind.Hybrid):
+        store = il.build(data, kind, il.Precision.double)
+        ref = oracle.predict(store, queries)
+        for s in ("tiled", "naive"):
+            got = il.STRATEGIES[s](store, queries, cfg=il.ExecConfig(mode="exact"))
+            both_nan = np.isnan(got) & np.isnan(ref)
+            assert np.array_equal(got[~both_nan].view(np.uint8), ref[~both_nan].view(np.uint8)), (scale, kind, s)
+            assert np.array_equal(np.isnan(got), np.isnan(ref)), (scale, kind, s)

@@ -14,8 +14,12 @@ T = {
     "naive_aoas": (100 * K, 100 * K, "aoas", "single", "naive", "fast"),
     "naive_soa": (100 * K, 100 * K, "soa", "single", "naive", "fast"),
     "naive_aos": (100 * K, 100 * K, "aos", "single", "naive", "fast"),
+    "tiled64_p35": (100 * K, 100 * K, "aoas", "double", "tiled", "fast"),
+    "c1": (10 * K, 10 * K, "soa", "single", "tiled", "fast"),
+    "c2": (100 * K, 100 * K, "aoas", "single", "tiled", "fast"),
+    "c5": (10240 * K, 100 * K, "aoas", "single", "tiled", "fast"),
 }
 name = sys.argv[1]
 args = T[name]
-p = 3.5 if name == "c4" else 2.0
+p = 3.5 if name in ("c4", "tiled64_p35") else 2.0
 run(*args, p=p, reps=1)
