@@ -413,7 +413,8 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             t_e2e = float(t.item())
         e = 4 if prec == "single" else 8
-        h2d = sum(b.nbytes for b in hstore.buffers) + 2 * (hi - lo) * e
+        # store buffers + the (m, 2) float64 query pairs (cast on the device, idw_run_xy)
+        h2d = sum(b.nbytes for b in hstore.buffers) + 16 * (hi - lo)
         d2h = (hi - lo) * e
         h2d_all, d2h_all = h2d, d2h
         if dist is not None:

@@ -69,7 +69,8 @@ enum idw_err {
   IDW_E_ARG = -1,         /* malformed argument (kind/precision/buffers/sizes)  */
   IDW_E_UNSUPPORTED = -2, /* illegal layout/precision pair or variant         */
   IDW_E_CUDA = -3,        /* CUDA runtime failure or no device                */
-  IDW_E_NOMEM = -4        /* device allocation failure                        */
+  IDW_E_NOMEM = -4,       /* device allocation failure                        */
+  IDW_E_NONFINITE = -5    /* a query coordinate is NaN/inf (core.ensure_finite) */
 };
 
 /* A point store == layouts.LayoutStore (layouts.py:143-170): kind, precision,
@@ -122,6 +123,17 @@ const char *idw_last_error(void);
  * Replaces one whole strategies.run_* call body.                          */
 int idw_run(const idw_store *store, const void *qx, const void *qy, int64_t m,
             const idw_params *prm, void *out, idw_stats *stats);
+
+/* Blocking run over HOST memory that takes the reference's own query array:
+ * `queries` holds m (x, y) float64 pairs, row-major -- what
+ * core.as_query_array (core.py:93-101) returns.  The rest of
+ * strategies._prepare (strategies.py:125-134) runs on the device: the
+ * finiteness test of core.ensure_finite (core.py:113-116) and the
+ * round-to-nearest cast to the run dtype.  A non-finite coordinate returns
+ * IDW_E_NONFINITE ("invalid coordinate"; `out` is then unspecified).
+ * Otherwise identical to idw_run.                                          */
+int idw_run_xy(const idw_store *store, const double *queries, int64_t m,
+               const idw_params *prm, void *out, idw_stats *stats);
 
 /* Asynchronous run over DEVICE memory on `stream` (a cudaStream_t, NULL =
  * legacy default stream).  Store buffers must stay readable up to

@@ -60,7 +60,7 @@ class IdwStats(ctypes.Structure):
     ]
 
 
-EXPORTS = ("idw_abi_version", "idw_device_count", "idw_last_error", "idw_run",
+EXPORTS = ("idw_abi_version", "idw_device_count", "idw_last_error", "idw_run", "idw_run_xy",
            "idw_run_device", "idw_pack_device", "idw_convert_device", "idw_last_kernel_ms",
            "idw_mufu_peak")
 
@@ -102,6 +102,9 @@ def load() -> ctypes.CDLL:
     lib.idw_run.restype = ctypes.c_int
     lib.idw_run.argtypes = [ctypes.POINTER(IdwStore), ptr, ptr, ctypes.c_int64,
                             ctypes.POINTER(IdwParams), ptr, ctypes.POINTER(IdwStats)]
+    lib.idw_run_xy.restype = ctypes.c_int
+    lib.idw_run_xy.argtypes = [ctypes.POINTER(IdwStore), ptr, ctypes.c_int64,
+                               ctypes.POINTER(IdwParams), ptr, ctypes.POINTER(IdwStats)]
     lib.idw_run_device.restype = ctypes.c_int
     lib.idw_run_device.argtypes = [ctypes.POINTER(IdwStore), ptr, ptr, ctypes.c_int64,
                                    ctypes.POINTER(IdwParams), ptr, ptr, ctypes.POINTER(IdwStats)]
@@ -162,6 +165,24 @@ def run_host(store: IdwStore, qx: np.ndarray, qy: np.ndarray, params: IdwParams,
     m = out.shape[0]
     _check(lib.idw_run(ctypes.byref(store), qx.ctypes.data, qy.ctypes.data, m,
                        ctypes.byref(params), out.ctypes.data, ctypes.byref(stats)))
+    return stats
+
+
+E_NONFINITE = -5  # include/idw_b200.h
+
+
+def run_host_xy(store: IdwStore, queries: np.ndarray, params: IdwParams, out: np.ndarray) -> IdwStats:
+    """Blocking ``idw_run_xy``: the (m, 2) float64 C-contiguous query array of
+    core.as_query_array goes to the device as is; the cast to the run dtype
+    and core.ensure_finite's test run there.  A non-finite coordinate raises
+    ValueError("invalid coordinate") like the reference (core.py:113-116)."""
+    lib = load()
+    stats = IdwStats()
+    rc = lib.idw_run_xy(ctypes.byref(store), queries.ctypes.data, out.shape[0], ctypes.byref(params),
+                        out.ctypes.data, ctypes.byref(stats))
+    if rc == E_NONFINITE:
+        raise ValueError("invalid coordinate")
+    _check(rc)
     return stats
 
 

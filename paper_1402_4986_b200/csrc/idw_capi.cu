@@ -253,19 +253,18 @@ int idw_run_device(const idw_store *s, const void *qx, const void *qy, int64_t m
   return rc;
 }
 
-int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p, void *out,
-            idw_stats *stats) {
-  g_err.clear();
-  int rc = validate(s, qx, qy, m, p, out);
-  if (rc) return rc;
-  if (m == 0) return 0;
+// Host-buffer path shared by idw_run (cast qx/qy given) and idw_run_xy (the
+// reference's (m, 2) float64 query array, split + cast + checked on device).
+static int run_host(const idw_store *s, const void *qx, const void *qy, const double *xy, int64_t m,
+                    const idw_params *p, void *out, idw_stats *stats) {
   cudaStream_t st;
-  int sms;
+  int sms, rc;
   if ((rc = device_stream(p->device, &st, &sms))) return rc;
   const size_t esz = s->precision == IDW_SINGLE ? 4 : 8;
   // one stream-ordered arena: buffers (padded to 16 B + 64 B slack for the
-  // rounded-up bulk copy of the tail tile), qx, qy, out, flags, fix-up counter
-  size_t off[8], total = 0;
+  // rounded-up bulk copy of the tail tile), qx, qy, out, flags, fix-up
+  // counter, non-finite flag, raw xy pairs
+  size_t off[10], total = 0;
   auto take = [&](size_t bytes) {
     size_t o = total;
     total += (bytes + 255) & ~size_t(255);
@@ -277,6 +276,8 @@ int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const
   off[5] = take(esz * (size_t)m);
   off[6] = take((size_t)m);
   off[7] = take(sizeof(unsigned long long));
+  off[8] = take(sizeof(unsigned int));
+  off[9] = xy ? take(2 * sizeof(double) * (size_t)m) : 0;
   unsigned char *arena = nullptr;
   IDW_CK(cudaMallocAsync((void **)&arena, total, st));
   const void *dbuf[3] = {nullptr, nullptr, nullptr};
@@ -284,9 +285,17 @@ int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const
     IDW_CK(cudaMemcpyAsync(arena + off[b], s->buf[b], (size_t)s->nbytes[b], cudaMemcpyHostToDevice, st));
     dbuf[b] = arena + off[b];
   }
-  IDW_CK(cudaMemcpyAsync(arena + off[3], qx, esz * (size_t)m, cudaMemcpyHostToDevice, st));
-  IDW_CK(cudaMemcpyAsync(arena + off[4], qy, esz * (size_t)m, cudaMemcpyHostToDevice, st));
-  IDW_CK(cudaMemsetAsync(arena + off[7], 0, sizeof(unsigned long long), st));
+  unsigned int *bad = (unsigned int *)(arena + off[8]);
+  IDW_CK(cudaMemsetAsync(arena + off[7], 0, 256 + 256, st));  // nfixed + bad (adjacent 256-B slots)
+  if (xy) {
+    IDW_CK(cudaMemcpyAsync(arena + off[9], xy, 2 * sizeof(double) * (size_t)m, cudaMemcpyHostToDevice, st));
+    if ((rc = split_queries((const double *)(arena + off[9]), m, s->precision, arena + off[3], arena + off[4], bad,
+                            st, sms)))
+      return rc;
+  } else {
+    IDW_CK(cudaMemcpyAsync(arena + off[3], qx, esz * (size_t)m, cudaMemcpyHostToDevice, st));
+    IDW_CK(cudaMemcpyAsync(arena + off[4], qy, esz * (size_t)m, cudaMemcpyHostToDevice, st));
+  }
   Launch L;
   fill_launch(L, s, dbuf, arena + off[3], arena + off[4], m, p, arena + off[5]);
   L.st = st;
@@ -299,11 +308,13 @@ int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const
   IDW_CK(cudaEventCreate(&e1));
   IDW_CK(cudaEventRecord(e0, st));
   rc = dispatch(L);
+  unsigned int nonfinite = 0;
   if (rc == 0) {
     IDW_CK(cudaEventRecord(e1, st));
     IDW_CK(cudaMemcpyAsync(out, arena + off[5], esz * (size_t)m, cudaMemcpyDeviceToHost, st));
     unsigned long long nfix = 0;
     IDW_CK(cudaMemcpyAsync(&nfix, L.nfixed, sizeof(nfix), cudaMemcpyDeviceToHost, st));
+    IDW_CK(cudaMemcpyAsync(&nonfinite, bad, sizeof(nonfinite), cudaMemcpyDeviceToHost, st));
     IDW_CK(cudaStreamSynchronize(st));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
@@ -317,7 +328,28 @@ int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   fill_stats(stats, L, p, s->count, m);
+  if (rc == 0 && nonfinite) {
+    set_error("invalid coordinate");  // core.ensure_finite (core.py:113-116)
+    return IDW_E_NONFINITE;
+  }
   return rc;
+}
+
+int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p, void *out,
+            idw_stats *stats) {
+  g_err.clear();
+  int rc = validate(s, qx, qy, m, p, out);
+  if (rc) return rc;
+  if (m == 0) return 0;
+  return run_host(s, qx, qy, nullptr, m, p, out, stats);
+}
+
+int idw_run_xy(const idw_store *s, const double *xy, int64_t m, const idw_params *p, void *out, idw_stats *stats) {
+  g_err.clear();
+  int rc = validate(s, xy, xy, m, p, out);
+  if (rc) return rc;
+  if (m == 0) return 0;
+  return run_host(s, nullptr, nullptr, xy, m, p, out, stats);
 }
 
 // Shape check of a destination/source store against the layout table.

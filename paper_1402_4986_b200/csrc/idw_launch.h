@@ -118,6 +118,10 @@ int pack_device(const double *x, const double *y, const double *z, long long n, 
 int convert_device(const unsigned char *const *src, int kin, unsigned char *const *dst, int kout, int prec,
                    long long n, cudaStream_t st, int sms);
 
+// (m, 2) float64 query pairs -> qx, qy in the run dtype + non-finite flag.
+int split_queries(const double *xy, long long m, int prec, void *qx, void *qy, unsigned int *bad, cudaStream_t st,
+                  int sms);
+
 // Does this launch write screen flags and need the fix-up pass?
 inline bool needs_fixup(const Launch &L) {
   if (L.variant == IDW_NESTED_ORIGINAL) return false;

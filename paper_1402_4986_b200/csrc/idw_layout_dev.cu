@@ -126,4 +126,33 @@ int convert_device(const unsigned char *const *src, int kin, unsigned char *cons
   });
 }
 
+// strategies._prepare on the device (strategies.py:125-134): the reference's
+// (m, 2) float64 query array -> contiguous qx, qy in the run dtype (cast
+// round-to-nearest, like numpy astype), with core.ensure_finite's test
+// (core.py:113-116) folded into one flag word.
+template <typename T>
+__global__ void __launch_bounds__(256) k_split_queries(const double2 *__restrict__ xy, long long m,
+                                                      T *__restrict__ qx, T *__restrict__ qy,
+                                                      unsigned int *__restrict__ bad) {
+  bool nf = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
+    const double2 v = xy[i];
+    nf |= !isfinite(v.x) || !isfinite(v.y);
+    qx[i] = (T)v.x;
+    qy[i] = (T)v.y;
+  }
+  if (__any_sync(0xffffffffu, nf) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
+int split_queries(const double *xy, long long m, int prec, void *qx, void *qy, unsigned int *bad, cudaStream_t st,
+                  int sms) {
+  const double2 *src = reinterpret_cast<const double2 *>(xy);
+  if (prec == IDW_SINGLE)
+    k_split_queries<float><<<grid_for(m, sms), 256, 0, st>>>(src, m, (float *)qx, (float *)qy, bad);
+  else
+    k_split_queries<double><<<grid_for(m, sms), 256, 0, st>>>(src, m, (double *)qx, (double *)qy, bad);
+  IDW_CK_LAUNCH();
+  return 0;
+}
+
 }  // namespace idw

@@ -151,13 +151,25 @@ def _native_store(store) -> _capi.IdwStore:
 
 
 def _dispatch(variant: str, store, queries, params: Params, cfg: ExecConfig):
-    qx, qy, dt = _prepare(store, queries, params)
-    out = np.empty(qx.shape[0], dtype=dt)
-    if out.shape[0] == 0:
-        return out, None
+    """One blocking native call.  The query array goes to the device as the
+    reference's (m, 2) float64 pairs (idw_run_xy): the finiteness test and the
+    run-dtype cast of _prepare run there, with the same ValueError."""
+    qs = as_query_array(queries)
+    dt = np.dtype(np.float64 if store.precision.value == "double" else np.float32)
+    if store.count == 0 or qs.shape[0] == 0:
+        _prepare(store, qs, params)  # reference order: invalid coordinate, then no data points
+        return np.empty(qs.shape[0], dtype=dt), None
+    qs = np.ascontiguousarray(qs)
+    out = np.empty(qs.shape[0], dtype=dt)
     prm = _capi.make_params(params.p, params.zero_eps, variant, cfg.mode, cfg.group_size,
                             cfg.tile_size, cfg.splits, cfg.device)
-    stats = _capi.run_host(_native_store(store), qx, qy, prm, out)
+    try:
+        stats = _capi.run_host_xy(_native_store(store), qs, prm, out)
+    except _capi.NativeError:
+        # the input's own error outranks a device failure (e.g. no GPU):
+        # report what the reference would raise, if anything
+        _prepare(store, qs, params)
+        raise
     return out, stats
 
 

@@ -360,3 +360,30 @@ def test_exact_fp64_scales_bitwise(il, scale):
             both_nan = np.isnan(got) & np.isnan(ref)
             assert np.array_equal(got[~both_nan].view(np.uint8), ref[~both_nan].view(np.uint8)), (scale, kind, s)
             assert np.array_equal(np.isnan(got), np.isnan(ref)), (scale, kind, s)
+
+
+def test_device_side_prepare_matches_host_cast(il):
+    """idw_run_xy (the (m, 2) float64 queries split, cast RN and checked on the
+    device) == idw_run over the host-cast qx, qy (strategies._prepare), bitwise;
+    a NaN or inf anywhere raises the reference's ValueError."""
+    from paper_1402_4986_b200 import _capi, strategies
+
+    rng = np.random.default_rng(71)
+    data = random_records(rng, 5000)
+    queries = random_queries(rng, 3001) * 3.0 - 1.0
+    for kind, precision in (("aoas", il.Precision.single), ("soa", il.Precision.double)):
+        store = il.build(data, il.LayoutKind(kind), precision)
+        for variant in ("tiled", "naive", "nested_improved"):
+            for mode in ("exact", "fast"):
+                prm = _capi.make_params(2.0, 0.0, variant, mode, 1024, 1024)
+                qx, qy, dt = strategies._prepare(store, queries, il.Params())
+                a = np.empty(len(queries), dt)
+                _capi.run_host(strategies._native_store(store), qx, qy, prm, a)
+                b = np.empty(len(queries), dt)
+                _capi.run_host_xy(strategies._native_store(store), np.ascontiguousarray(queries), prm, b)
+                assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (kind, variant, mode)
+        for bad in (np.nan, np.inf, -np.inf):
+            q = queries.copy()
+            q[1234, 1] = bad
+            with pytest.raises(ValueError, match="invalid coordinate"):
+                il.run_tiled(store, q)
