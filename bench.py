@@ -9,7 +9,8 @@ from the reference's splitmix64 generator (data seed 0, query seed 1).  One
 step = one whole job: broadcast of the data buffers from rank 0 (N > 1), every
 rank's query shard through K2 + fix-up, gather of the predictions.
 
-`value` is whole-job pairs/s with inputs resident in HBM (CUDA events on the
+`value` is whole-job pairs/s with inputs resident in HBM, each step one replay
+of a CUDA-graph plan of the call (idw_plan_*; CUDA events on the
 launching stream, barrier + synchronize on both sides, max over ranks); `e2e`
 is the same metric through the public drop-in API (`run_tiled` on host arrays:
 H2D of store + queries and D2H of the predictions inside the timed region).
@@ -215,7 +216,7 @@ def run_ours(args):
 
     import paper_1402_4986_b200 as il
     from paper_1402_4986_b200 import _capi
-    from paper_1402_4986_b200.device import DeviceStore, predict_device
+    from paper_1402_4986_b200.device import DevicePlan, DeviceStore
     from paper_1402_4986_b200.partition import QueryShardedRunner, StoreMeta, shard_bounds
 
     world, rank, local = dist_env()
@@ -266,19 +267,24 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     launches = [0]
 
-    def step():
+    # One CUDA-graph plan per timed step (idw_plan: bbox pre-pass + variant
+    # kernels + fix-up captured once, replayed with one graph launch); each
+    # plan's timing event nodes then hold its own step's kernel time.
+    plans = [DevicePlan(dstore, qx_l, qy_l, out_l, params, cfg, variant) for _ in range(max(args.steps, 1))]
+
+    def step(plan):
         if runner is not None:
             for t in bufs:  # the data replication collective (NVLink/NVSwitch)
                 dist.broadcast(t, src=0)
-        st = predict_device(dstore, qx_l, qy_l, out_l, params, cfg, variant, stream)
-        launches[0] += int(st.kernel_launches)
+        plan.launch(stream)
+        launches[0] += plan.launches
         if runner is not None:
             runner.gather(out_l, m)
 
     # ---- MUFU roofline probe (same GPU, just before the timed region)
     probe_rate, probe_hz = _capi.mufu_peak(local)
-    for _ in range(args.warmup):
-        step()
+    for w in range(max(args.warmup, len(plans))):  # every plan replays at least once before timing
+        step(plans[w % len(plans)])
         flush.zero_()
     torch.cuda.synchronize(dev)
     props = torch.cuda.get_device_properties(dev)
@@ -297,7 +303,7 @@ def run_ours(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for k in range(args.steps):
         ev[k][0].record(stream)
-        step()
+        step(plans[k])
         ev[k][1].record(stream)
         flush.zero_()
     torch.cuda.synchronize(dev)
@@ -305,7 +311,7 @@ def run_ours(args):
         dist.barrier()
     clocks = sampler.stop()
     ms_local = sum(a.elapsed_time(b) for a, b in ev)
-    kern = [_capi.last_kernel_ms()]  # events inside the library around the last step's kernels
+    kern = [pl.kernel_ms() for pl in plans[:args.steps]]  # event nodes inside each step's graph
     ms = ms_local
     if dist is not None:
         t = torch.tensor([ms_local], device=dev, dtype=torch.float64)

@@ -142,6 +142,23 @@ int idw_run_xy(const idw_store *store, const double *queries, int64_t m,
 int idw_run_device(const idw_store *store, const void *qx, const void *qy, int64_t m,
                    const idw_params *prm, void *out, void *stream, idw_stats *stats);
 
+/* Plans: one idw_run_device call captured into a CUDA graph (the bounding-box
+ * pre-pass, the variant kernels, the fix-up pass and their stream-ordered
+ * scratch), replayed by idw_plan_launch for ~3 us of host time instead of
+ * one runtime call per kernel.  The plan keeps the store, query and output
+ * DEVICE pointers it was created with: refill qx/qy (or the store) in place
+ * between launches.  Launches of one plan must not overlap each other.    */
+typedef struct idw_plan idw_plan;
+int idw_plan_create(const idw_store *store, const void *qx, const void *qy, int64_t m,
+                    const idw_params *prm, void *out, idw_plan **plan);
+int idw_plan_launch(idw_plan *plan, void *stream);
+/* Kernels one launch of the plan runs. */
+int64_t idw_plan_launches(const idw_plan *plan);
+/* Device time of the variant kernels and the fix-up pass of the plan's most
+ * recent launch (timing event nodes inside the graph); blocks until done.  */
+int idw_plan_kernel_ms(idw_plan *plan, double *variant_ms, double *fixup_ms);
+void idw_plan_destroy(idw_plan *plan);
+
 /* Device-side layout packer: fp64 component arrays x, y, z (n device values
  * each) cast round-to-nearest to the store's precision and written into the
  * preallocated device buffers of `dst` in its layout, pads zeroed -- the

@@ -62,7 +62,8 @@ class IdwStats(ctypes.Structure):
 
 EXPORTS = ("idw_abi_version", "idw_device_count", "idw_last_error", "idw_run", "idw_run_xy",
            "idw_run_device", "idw_pack_device", "idw_convert_device", "idw_last_kernel_ms",
-           "idw_mufu_peak")
+           "idw_mufu_peak", "idw_plan_create", "idw_plan_launch", "idw_plan_launches",
+           "idw_plan_kernel_ms", "idw_plan_destroy")
 
 
 class NativeError(RuntimeError):
@@ -117,6 +118,17 @@ def load() -> ctypes.CDLL:
     lib.idw_mufu_peak.restype = ctypes.c_int
     lib.idw_mufu_peak.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double)]
+    lib.idw_plan_create.restype = ctypes.c_int
+    lib.idw_plan_create.argtypes = [ctypes.POINTER(IdwStore), ptr, ptr, ctypes.c_int64,
+                                    ctypes.POINTER(IdwParams), ptr, ctypes.POINTER(ctypes.c_void_p)]
+    lib.idw_plan_launch.restype = ctypes.c_int
+    lib.idw_plan_launch.argtypes = [ptr, ptr]
+    lib.idw_plan_launches.restype = ctypes.c_int64
+    lib.idw_plan_launches.argtypes = [ptr]
+    lib.idw_plan_kernel_ms.restype = ctypes.c_int
+    lib.idw_plan_kernel_ms.argtypes = [ptr, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    lib.idw_plan_destroy.restype = None
+    lib.idw_plan_destroy.argtypes = [ptr]
     _lib = lib
     return lib
 
@@ -211,6 +223,39 @@ def last_kernel_ms() -> tuple[float, float]:
     b = ctypes.c_double()
     _check(load().idw_last_kernel_ms(ctypes.byref(a), ctypes.byref(b)))
     return a.value, b.value
+
+
+class Plan:
+    """An ``idw_plan``: one run_device call captured into a CUDA graph over
+    fixed device pointers, replayed by :meth:`launch`."""
+
+    def __init__(self, store: IdwStore, qx_ptr: int, qy_ptr: int, m: int, params: IdwParams, out_ptr: int):
+        self._lib = load()
+        h = ctypes.c_void_p()
+        _check(self._lib.idw_plan_create(ctypes.byref(store), qx_ptr, qy_ptr, m, ctypes.byref(params),
+                                         out_ptr, ctypes.byref(h)))
+        self._h = h
+        self.launches = int(self._lib.idw_plan_launches(h))
+
+    def launch(self, stream: int = 0) -> None:
+        _check(self._lib.idw_plan_launch(self._h, stream))
+
+    def kernel_ms(self) -> tuple[float, float]:
+        a = ctypes.c_double()
+        b = ctypes.c_double()
+        _check(self._lib.idw_plan_kernel_ms(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.idw_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def mufu_peak(device: int = 0) -> tuple[float, float]:

@@ -178,9 +178,11 @@ struct EvSet {
 static thread_local EvSet g_ev[64];
 static thread_local int g_last_dev = -1;
 
-static int dispatch(Launch &L, const EvSet *ev = nullptr) {
+// evflags: cudaEventRecordExternal when the stream is being captured into a
+// graph (the records become timing-capable event nodes of the graph).
+static int dispatch(Launch &L, const EvSet *ev = nullptr, unsigned evflags = cudaEventRecordDefault) {
   int rc = 0;
-  if (ev) IDW_CK(cudaEventRecord(ev->a, L.st));
+  if (ev) IDW_CK(cudaEventRecordWithFlags(ev->a, L.st, evflags));
   switch (L.variant) {
     case IDW_NAIVE: rc = launch_naive(L); break;
     case IDW_TILED: rc = launch_tiled(L); break;
@@ -189,10 +191,10 @@ static int dispatch(Launch &L, const EvSet *ev = nullptr) {
     default: set_error("unknown variant"); return IDW_E_ARG;
   }
   if (rc) return rc;
-  if (ev) IDW_CK(cudaEventRecord(ev->b, L.st));
+  if (ev) IDW_CK(cudaEventRecordWithFlags(ev->b, L.st, evflags));
   if (needs_fixup(L)) rc = launch_fixup(L);
   if (rc) return rc;
-  if (ev) IDW_CK(cudaEventRecord(ev->c, L.st));
+  if (ev) IDW_CK(cudaEventRecordWithFlags(ev->c, L.st, evflags));
   return rc;
 }
 
@@ -203,6 +205,15 @@ static void fill_stats(idw_stats *st, const Launch &L, const idw_params *p, int6
 }
 
 }  // namespace idw
+
+// A captured idw_run_device call (include/idw_b200.h: idw_plan_*).
+struct idw_plan {
+  int dev = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  idw::EvSet ev;
+  int64_t launches = 0;
+};
 
 using namespace idw;
 
@@ -333,6 +344,105 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
     return IDW_E_NONFINITE;
   }
   return rc;
+}
+
+static void plan_free(idw_plan *pl) {
+  if (!pl) return;
+  if (pl->exec) cudaGraphExecDestroy(pl->exec);
+  if (pl->graph) cudaGraphDestroy(pl->graph);
+  if (pl->ev.a) cudaEventDestroy(pl->ev.a);
+  if (pl->ev.b) cudaEventDestroy(pl->ev.b);
+  if (pl->ev.c) cudaEventDestroy(pl->ev.c);
+  delete pl;
+}
+
+int idw_plan_create(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p, void *out,
+                    idw_plan **plan) {
+  g_err.clear();
+  if (!plan) return set_error("null plan pointer"), IDW_E_ARG;
+  *plan = nullptr;
+  int rc = validate(s, qx, qy, m, p, out);
+  if (rc) return rc;
+  if (m == 0) return set_error("a plan needs at least one query"), IDW_E_ARG;
+  cudaStream_t dst;
+  int sms;
+  if ((rc = device_stream(p->device, &dst, &sms))) return rc;
+  idw_plan *pl = new idw_plan();
+  pl->dev = p->device;
+  cudaStream_t cap = nullptr;
+  auto fail = [&](int code) {
+    if (cap) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(cap, &g);  // abandon a half-built capture
+      if (g) cudaGraphDestroy(g);
+      cudaStreamDestroy(cap);
+    }
+    cudaGetLastError();
+    plan_free(pl);
+    return code;
+  };
+  if (cudaEventCreate(&pl->ev.a) || cudaEventCreate(&pl->ev.b) || cudaEventCreate(&pl->ev.c))
+    return set_error("cudaEventCreate failed"), fail(IDW_E_CUDA);
+  if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess)
+    return set_error("cudaStreamCreate failed"), fail(IDW_E_CUDA);
+  if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed) != cudaSuccess)
+    return set_error("cudaStreamBeginCapture failed"), fail(IDW_E_CUDA);
+  Launch L;
+  fill_launch(L, s, s->buf, qx, qy, m, p, out);
+  L.st = cap;
+  L.dev = p->device;
+  L.sms = sms;
+  unsigned char *flags = nullptr;
+  if (needs_fixup(L)) {
+    if (cudaMallocAsync((void **)&flags, (size_t)m, cap) != cudaSuccess)
+      return set_error("cudaMallocAsync (captured) failed"), fail(IDW_E_CUDA);
+    L.flags = flags;
+  }
+  if ((rc = dispatch(L, &pl->ev, cudaEventRecordExternal))) return fail(rc);
+  if (flags) cudaFreeAsync(flags, cap);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(cap, &g);
+  cudaStreamDestroy(cap);
+  cap = nullptr;
+  if (ce != cudaSuccess || !g) return set_error(std::string("stream capture: ") + cudaGetErrorString(ce)), fail(IDW_E_CUDA);
+  pl->graph = g;
+  if (cudaGraphInstantiate(&pl->exec, g, 0) != cudaSuccess)
+    return set_error("cudaGraphInstantiate failed"), fail(IDW_E_CUDA);
+  // upload now so the first launch does not pay for it
+  if (cudaGraphUpload(pl->exec, dst) != cudaSuccess || cudaStreamSynchronize(dst) != cudaSuccess)
+    return set_error("cudaGraphUpload failed"), fail(IDW_E_CUDA);
+  pl->launches = L.launches;
+  *plan = pl;
+  return 0;
+}
+
+int idw_plan_launch(idw_plan *pl, void *stream) {
+  g_err.clear();
+  if (!pl || !pl->exec) return set_error("null plan"), IDW_E_ARG;
+  IDW_CK(cudaSetDevice(pl->dev));
+  IDW_CK(cudaGraphLaunch(pl->exec, (cudaStream_t)stream));
+  return 0;
+}
+
+int64_t idw_plan_launches(const idw_plan *pl) { return pl ? pl->launches : 0; }
+
+int idw_plan_kernel_ms(idw_plan *pl, double *variant_ms, double *fixup_ms) {
+  g_err.clear();
+  if (!pl) return set_error("null plan"), IDW_E_ARG;
+  IDW_CK(cudaSetDevice(pl->dev));
+  IDW_CK(cudaEventSynchronize(pl->ev.c));
+  float a = 0.f, b = 0.f;
+  IDW_CK(cudaEventElapsedTime(&a, pl->ev.a, pl->ev.b));
+  IDW_CK(cudaEventElapsedTime(&b, pl->ev.b, pl->ev.c));
+  if (variant_ms) *variant_ms = a;
+  if (fixup_ms) *fixup_ms = b;
+  return 0;
+}
+
+void idw_plan_destroy(idw_plan *pl) {
+  if (!pl) return;
+  cudaSetDevice(pl->dev);
+  plan_free(pl);
 }
 
 int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p, void *out,

@@ -165,3 +165,35 @@ def predict_device(dstore: DeviceStore, qx, qy, out, params: Params = Params(),
                             cfg.tile_size, cfg.splits, dstore.device)
     return _capi.run_device(dstore.native(), qx.data_ptr(), qy.data_ptr(), m, prm,
                             out.data_ptr(), stream.cuda_stream)
+
+
+class DevicePlan:
+    """``predict_device`` captured once into a CUDA graph (idw_plan_create) and
+    replayed per batch: the serving loop refills ``qx``/``qy`` in place and
+    calls :meth:`launch` -- one graph launch instead of a runtime call per
+    kernel.  Holds references to the tensors whose pointers the graph uses."""
+
+    def __init__(self, dstore: DeviceStore, qx, qy, out, params: Params = Params(),
+                 cfg: ExecConfig | None = None, variant: str = "tiled"):
+        cfg = cfg or ExecConfig()
+        self._keep = (dstore, qx, qy, out)
+        prm = _capi.make_params(params.p, params.zero_eps, variant, cfg.mode, cfg.group_size,
+                                cfg.tile_size, cfg.splits, dstore.device)
+        self._plan = _capi.Plan(dstore.native(), qx.data_ptr(), qy.data_ptr(), int(out.shape[0]), prm,
+                                out.data_ptr())
+        self.launches = self._plan.launches
+        self.device = dstore.device
+
+    def launch(self, stream=None) -> None:
+        import torch
+
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self._plan.launch(stream.cuda_stream)
+
+    def kernel_ms(self) -> tuple[float, float]:
+        """(variant kernels ms, fix-up ms) of the most recent launch."""
+        return self._plan.kernel_ms()
+
+    def close(self) -> None:
+        self._plan.close()

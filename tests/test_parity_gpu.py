@@ -387,3 +387,39 @@ def test_device_side_prepare_matches_host_cast(il):
             q[1234, 1] = bad
             with pytest.raises(ValueError, match="invalid coordinate"):
                 il.run_tiled(store, q)
+
+
+def test_plan_graph_replay_matches_run_device(il):
+    """idw_plan (the call captured into a CUDA graph) == idw_run_device,
+    bitwise, for every variant/mode; refilling the query tensors in place and
+    relaunching gives the new batch's predictions; timing nodes work."""
+    import torch
+
+    from paper_1402_4986_b200.device import DevicePlan, DeviceStore, predict_device
+
+    rng = np.random.default_rng(73)
+    data = random_records(rng, 30000)
+    qa, qb = random_queries(rng, 2500), random_queries(rng, 2500)
+    qa[7] = data[11, :2]  # a coincidence: the fix-up node must run inside the graph
+    for kind, precision in (("soa", il.Precision.single), ("aos", il.Precision.double)):
+        store = il.build(data, il.LayoutKind(kind), precision)
+        ds = DeviceStore(store, 0)
+        for variant in ("tiled", "naive", "nested_improved", "nested_original"):
+            for mode in ("exact", "fast"):
+                cfg = il.ExecConfig(mode=mode, group_size=512)
+                q = [torch.tensor(qa[:, k].astype(precision.dtype), device="cuda") for k in (0, 1)]
+                out = torch.empty(len(qa), dtype=ds.dtype, device="cuda")
+                plan = DevicePlan(ds, q[0], q[1], out, il.Params(), cfg, variant)
+                assert plan.launches >= 1
+                plan.launch()
+                ms, _ = plan.kernel_ms()
+                assert ms > 0
+                ref = torch.empty_like(out)
+                predict_device(ds, q[0], q[1], ref, il.Params(), cfg, variant)
+                assert torch.equal(out.view(torch.uint8), ref.view(torch.uint8)), (kind, variant, mode)
+                for k in (0, 1):
+                    q[k].copy_(torch.tensor(qb[:, k].astype(precision.dtype)))
+                plan.launch()
+                predict_device(ds, q[0], q[1], ref, il.Params(), cfg, variant)
+                assert torch.equal(out.view(torch.uint8), ref.view(torch.uint8)), (kind, variant, mode, "refill")
+                plan.close()
