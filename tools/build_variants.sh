@@ -6,13 +6,14 @@ cd "$(dirname "$0")/../paper_1402_4986_b200/csrc"
 NVFLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr"
 OUT=../../build/variants
 mkdir -p $OUT
-for v in "$@"; do   # v = Q,U
-  q=${v%,*}; u=${v#*,}
-  nvcc $NVFLAGS -DIDW_NEST_Q64=$q -DIDW_NEST_U=$u -c idw_nested.cu -o $OUT/nested_q${q}_u${u}.o &
+# v = name:extra nvcc defines (comma separated), e.g. r0u8:-DIDW_NEST_RING32=0,-DIDW_NEST_U32=8
+for v in "$@"; do
+  name=${v%%:*}; defs=$(echo ${v#*:} | tr ',' ' ')
+  nvcc $NVFLAGS $defs -c idw_nested.cu -o $OUT/nested_$name.o &
 done
 wait
 for v in "$@"; do
-  q=${v%,*}; u=${v#*,}
-  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/lib_q${q}_u${u}.so \
-    build/idw_capi.o build/idw_naive.o build/idw_tiled.o build/idw_layout_dev.o $OUT/nested_q${q}_u${u}.o
+  name=${v%%:*}
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/lib_$name.so \
+    build/idw_capi.o build/idw_naive.o build/idw_tiled.o build/idw_layout_dev.o $OUT/nested_$name.o
 done

@@ -17,6 +17,12 @@ cases = [(1024 * K, 64 * K, "soa", "double", "nested_improved", 3.5),
          (102400, 102400, "aoas", "double", "tiled", 3.5)]
 if len(sys.argv) > 1 and sys.argv[1] == "full":
     cases = [(1024 * K, 1024 * K, "soa", "double", "nested_improved", 3.5)]
+if len(sys.argv) > 1 and sys.argv[1] == "fp32":
+    cases = [(102400, 102400, "aoas", "single", "nested_improved", 2.0),
+             (102400, 102400, "soa", "single", "nested_improved", 2.0),
+             (102400, 102400, "aos", "single", "nested_improved", 2.0),
+             (10240 * K, 25 * K, "aoas", "single", "nested_improved", 2.0),
+             (102400, 102400, "aoas", "single", "nested_improved", 3.5)]
 for n, m, kind, prec, variant, p in cases:
     x, y, z = il.generate_cloud_arrays(n, 0)
     qx, qy, _ = il.generate_cloud_arrays(m, 1)

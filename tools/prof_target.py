@@ -16,6 +16,7 @@ T = {
     "naive_aos": (100 * K, 100 * K, "aos", "single", "naive", "fast"),
     "tiled64_p35": (100 * K, 100 * K, "aoas", "double", "tiled", "fast"),
     "c1": (10 * K, 10 * K, "soa", "single", "tiled", "fast"),
+    "c2_nested": (100 * K, 100 * K, "aoas", "single", "nested_improved", "fast"),
     "c2": (100 * K, 100 * K, "aoas", "single", "tiled", "fast"),
     "c5": (10240 * K, 100 * K, "aoas", "single", "tiled", "fast"),
 }
