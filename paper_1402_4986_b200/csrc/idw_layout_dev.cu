@@ -81,6 +81,62 @@ __global__ void __launch_bounds__(256) k_convert(Bufs in, long long n, WBufs w) 
   }
 }
 
+// Record layouts whose per-thread stores are not one aligned vector per point
+// (AoS: 12/24-byte records written as 3 scalars; fp64 AoaS: two double2 at a
+// 32-byte stride) are written through shared memory: each thread builds its
+// record in a tile image, then the block streams the image out with 16-byte
+// stores, contiguous across the warp.  Byte-identical output (the image holds
+// the same bytes, pads included); measured 0.75-0.82 -> see tools/layout_bench.py.
+constexpr int STAGE_PTS = 256;
+template <int KO, typename T>
+constexpr bool staged_out() {
+  return KO == AOS || (KO == AOAS && sizeof(T) == 8);
+}
+template <int KO, typename T>
+__device__ __forceinline__ void flush_tile(const WBufs &w, long long base, int cnt, unsigned char *img) {
+  using LT = LayoutTraits<KO, T>;
+  static_assert(LT::nbuf == 1, "staged layouts have one buffer");
+  constexpr int bpp = LT::bpp(0);
+  const int bytes = cnt * bpp;
+  unsigned char *dst = w.b[0] + base * bpp;  // base * bpp is 16-B aligned (STAGE_PTS * bpp is)
+  const int v16 = bytes >> 4;
+  for (int k = threadIdx.x; k < v16; k += blockDim.x)
+    reinterpret_cast<uint4 *>(dst)[k] = reinterpret_cast<const uint4 *>(img)[k];
+  for (int k = (v16 << 4) + threadIdx.x; k < bytes; k += blockDim.x) dst[k] = img[k];
+}
+
+template <int K, typename T>
+__global__ void __launch_bounds__(STAGE_PTS) k_pack_staged(const double *__restrict__ x, const double *__restrict__ y,
+                                                          const double *__restrict__ z, long long n, WBufs w) {
+  __shared__ __align__(16) unsigned char img[STAGE_PTS * LayoutTraits<K, T>::bpp(0)];
+  const WBufs sw{{img, nullptr, nullptr}};
+  for (long long base = blockIdx.x * (long long)STAGE_PTS; base < n; base += (long long)gridDim.x * STAGE_PTS) {
+    const int cnt = (int)(n - base < STAGE_PTS ? n - base : STAGE_PTS);
+    const long long i = base + threadIdx.x;
+    if ((int)threadIdx.x < cnt) GStore<K, T>::put(sw, threadIdx.x, (T)x[i], (T)y[i], (T)z[i]);
+    __syncthreads();
+    flush_tile<K, T>(w, base, cnt, img);
+    __syncthreads();
+  }
+}
+
+template <int KI, int KO, typename T>
+__global__ void __launch_bounds__(STAGE_PTS) k_convert_staged(Bufs in, long long n, WBufs w) {
+  __shared__ __align__(16) unsigned char img[STAGE_PTS * LayoutTraits<KO, T>::bpp(0)];
+  const WBufs sw{{img, nullptr, nullptr}};
+  for (long long base = blockIdx.x * (long long)STAGE_PTS; base < n; base += (long long)gridDim.x * STAGE_PTS) {
+    const int cnt = (int)(n - base < STAGE_PTS ? n - base : STAGE_PTS);
+    if ((int)threadIdx.x < cnt) {
+      T x, y, z;
+      GFetch<KI, T>::get(in, base + threadIdx.x, x, y, z);
+      GStore<KO, T>::put(sw, threadIdx.x, x, y, z);
+    }
+    __syncthreads();
+    flush_tile<KO, T>(w, base, cnt, img);
+    __syncthreads();
+  }
+}
+
 static int grid_for(long long n, int sms) {
   return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, (long long)sms * 16));
 }
@@ -100,7 +156,14 @@ int pack_device(const double *x, const double *y, const double *z, long long n, 
   return visit_kind(kind, prec, [&](auto KC, auto tv) -> int {
     using T = decltype(tv);
     constexpr int K = decltype(KC)::value;
-    k_pack<K, T><<<grid_for(n, sms), 256, 0, st>>>(x, y, z, n, w);
+    bool done = false;
+    if constexpr (staged_out<K, T>()) {
+      if (((uintptr_t)w.b[0] & 15) == 0) {  // 16-byte stores need an aligned buffer
+        k_pack_staged<K, T><<<grid_for(n, sms), STAGE_PTS, 0, st>>>(x, y, z, n, w);
+        done = true;
+      }
+    }
+    if (!done) k_pack<K, T><<<grid_for(n, sms), 256, 0, st>>>(x, y, z, n, w);
     IDW_CK_LAUNCH();
     return 0;
   });
@@ -116,7 +179,14 @@ int convert_device(const unsigned char *const *src, int kin, unsigned char *cons
     return visit_kind(kout, prec, [&](auto KOC, auto tv2) -> int {
       constexpr int KO = decltype(KOC)::value;
       if constexpr (std::is_same<T, decltype(tv2)>::value) {
-        k_convert<KI, KO, T><<<grid_for(n, sms), 256, 0, st>>>(in, n, w);
+        bool done = false;
+        if constexpr (staged_out<KO, T>()) {
+          if (((uintptr_t)w.b[0] & 15) == 0) {
+            k_convert_staged<KI, KO, T><<<grid_for(n, sms), STAGE_PTS, 0, st>>>(in, n, w);
+            done = true;
+          }
+        }
+        if (!done) k_convert<KI, KO, T><<<grid_for(n, sms), 256, 0, st>>>(in, n, w);
         IDW_CK_LAUNCH();
         return 0;
       } else {
