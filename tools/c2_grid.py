@@ -14,13 +14,15 @@ from paper_1402_4986_b200.device import DeviceStore, predict_device
 n = m = 100 * 1024
 x, y, z = il.generate_cloud_arrays(n, 0)
 qx, qy, _ = il.generate_cloud_arrays(m, il.query_seed(0))
-modes = sys.argv[1:] or ["fast", "exact"]
+modes = [a for a in sys.argv[1:] if a in ("fast", "exact")] or ["fast", "exact"]
+VARIANTS = ("naive", "tiled", "nested_improved", "nested_original") if "orig" in sys.argv else \
+    ("naive", "tiled", "nested_improved")
 for kind, prec in il.legal_pairs():
     st = il.LayoutStore.from_arrays(x, y, z, kind, prec)
     ds = DeviceStore(st, 0)
     tq = [torch.tensor(a.astype(prec.dtype), device="cuda") for a in (qx, qy)]
     out = torch.empty(m, dtype=ds.dtype, device="cuda")
-    for variant in ("naive", "tiled", "nested_improved"):
+    for variant in VARIANTS:
         for mode in modes:
             cfg = il.ExecConfig(mode=mode)
             predict_device(ds, tq[0], tq[1], out, il.Params(), cfg, variant)
