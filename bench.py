@@ -373,8 +373,16 @@ def run_ours(args):
             "mufu_per_pair": 7.0 / 8.0, "peak": mix_peak, "frac": achieved / mix_peak,
             "note": "MUFU ceiling of k_tiled's own instruction mix (shared reciprocal for 1 of 4 query pairs)"}
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
-    prof = ROOT / "profiles" / "r1" / f"prof_{args.config}_tiled.raw.csv"
-    if prof.exists() and args.mode == "fast":
+    # Algorithmic (compulsory) bytes of one launch: the store, the cast query
+    # coordinates in, the predictions out -- n*S_rec + 3*m_shard*e.
+    e_sz = 4 if prec == "single" else 8
+    srec = {"soa": 3 * e_sz, "aos": 3 * e_sz, "aoas": 4 * e_sz, "soaos": 32, "hybrid": 24}[layout]
+    roof["algorithmic_bytes"] = float(n * srec + 3 * (hi - lo) * e_sz)
+    # DRAM traffic of the dominant kernel from the committed ncu --set full
+    # capture of the same configuration (tools/gpu_round_final.sh)
+    caps = {"c1": "prof_c1", "c2": "prof_c2", "c3": "prof_c3_tiled", "c5": "prof_c5"}
+    prof = ROOT / "profiles" / "r1" / f"{caps.get(args.config, '-')}.raw.csv"
+    if prof.exists() and args.mode == "fast" and world == 1:
         import csv
 
         rows = list(csv.reader(open(prof)))
@@ -382,10 +390,14 @@ def run_ours(args):
         u = dict(zip(rows[0], rows[1]))
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         try:
-            tb = sum(float(d[k]) * scale[u[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-            roof["traffic"] = tb
-            roof["traffic_source"] = f"{prof.relative_to(ROOT)} (ncu --set full, one launch, same config)"
-            roof["algorithmic_bytes"] = float(n * (16 if layout == "aoas" else 12) + 2 * (hi - lo) * 4)
+            rd = float(d["dram__bytes_read.sum"]) * scale[u["dram__bytes_read.sum"]]
+            wr = float(d["dram__bytes_write.sum"]) * scale[u["dram__bytes_write.sum"]]
+            roof["traffic"] = rd + wr
+            roof["traffic_read"] = rd
+            roof["traffic_write"] = wr
+            roof["traffic_source"] = f"{prof.relative_to(ROOT)} (ncu --set full, one k_tiled launch, same config)"
+            roof["traffic_note"] = ("writes above the algorithmic bytes are the per-split partial sums of the "
+                                    "data-split grid (splits x m x 17 B, folded by k_combine), not re-reads")
         except (KeyError, ValueError):
             pass
 
