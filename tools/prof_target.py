@@ -21,6 +21,9 @@ T = {
     "c5": (10240 * K, 100 * K, "aoas", "single", "tiled", "fast"),
 }
 name = sys.argv[1]
+if name.startswith("c2tiled:"):  # c2tiled:<layout>:<precision>
+    _, kind, prec = name.split(":")
+    T[name] = (100 * K, 100 * K, kind, prec, "tiled", "fast")
 args = T[name]
 p = 3.5 if name in ("c4", "tiled64_p35") else 2.0
 run(*args, p=p, reps=1)
