@@ -90,7 +90,8 @@ int launch_tiled(Launch &L) {
       constexpr int MODE = decltype(MC)::value;
       constexpr bool P2 = decltype(PC)::value, EPS = decltype(EC)::value;
       using C = TiledCfg<T, MODE>;
-      constexpr int Q = C::Q, TILE = C::TILE;
+      auto run_q = [&](auto QC) -> int {
+      constexpr int Q = decltype(QC)::value, TILE = C::TILE;
       constexpr int RING = tiled_ring_bytes<K, T, TILE>();
       auto kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE>;
       bool prod_used = false;
@@ -160,6 +161,18 @@ int launch_tiled(Launch &L) {
         IDW_CK(cudaFreeAsync(ws, L.st));
       }
       return 0;
+      };
+      if constexpr (std::is_same<T, float>::value && MODE == EXACT && P2 && !EPS) {
+        // EXACT keeps the strict data order, so it cannot split the data: when
+        // Q = 4 blocks would not cover the SMs once, halve the queries per
+        // thread so the same queries spread over all SMs (C2, 100K queries:
+        // 100 CTAs on 148 SMs -> 296 CTAs).  Per-query arithmetic unchanged.
+        // Measured at C2: SoA 2093 -> 2609, AoaS 2240 -> 2645 GPairs/s; AoS
+        // 2211 -> 2023, so AoS keeps Q = 4.  IDW_EXACT_Q2=0 disables.
+        static const int q2 = [] { const char *e = getenv("IDW_EXACT_Q2"); return e ? atoi(e) : 1; }();
+        if (K != AOS && q2 && cdiv(L.m, (long long)C::Q * C::NC_MAX) < L.sms) return run_q(IC<2>{});
+      }
+      return run_q(IC<C::Q>{});
     });
   });
 }
