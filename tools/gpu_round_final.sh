@@ -11,7 +11,10 @@ done
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_reference_c3.json 2>&1
 timeout 600 ncu --clock-control none --metrics gpu__time_duration.sum --csv --log-file $OUT/launches_bench.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1
-timeout 1200 python tools/c2_grid.py > $OUT/c2_grid.jsonl 2> $OUT/c2_grid.err
+timeout 1500 python tools/c2_grid.py orig > $OUT/c2_grid.jsonl 2> $OUT/c2_grid.err
+timeout 600 python tools/layout_bench.py > $OUT/layout_bench.jsonl 2> $OUT/layout_bench.err
+timeout 1200 python -m pytest tests -q -m gpu --timeout 900 > $OUT/pytest_gpu.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1
 timeout 600 python tools/shard_perf.py > $OUT/shard_perf.jsonl 2>&1
 cap() {  # name kernel-regex target
   timeout 900 ncu --clock-control none --set full --import-source on -k regex:$2 -s 1 -c 1 -o $OUT/$1 \
