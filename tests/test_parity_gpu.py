@@ -423,3 +423,22 @@ def test_plan_graph_replay_matches_run_device(il):
                 predict_device(ds, q[0], q[1], ref, il.Params(), cfg, variant)
                 assert torch.equal(out.view(torch.uint8), ref.view(torch.uint8)), (kind, variant, mode, "refill")
                 plan.close()
+
+
+def test_split_reduce_persistent_clusters(il):
+    """K3 at a size where every persistent cluster walks many query groups
+    (20K queries / 8 per team >> resident clusters) and the ring of the next
+    group is primed during the tree: FAST within 1e-5 of the truth (fp32) /
+    1e-12 (fp64), EXACT bitwise equal to the reference's nested_improved."""
+    rng = np.random.default_rng(79)
+    data = random_records(rng, 150_000)
+    queries = random_queries(rng, 20_000)
+    sub = np.arange(0, 20_000, 97)
+    for precision in il.Precision:
+        store = il.build(data, il.LayoutKind.AoaS, precision)
+        truth = oracle.truth(store, queries[sub])
+        fast = il.run_nested_improved(store, queries, cfg=il.ExecConfig(mode="fast"))
+        assert np.all(np.isfinite(fast))
+        assert rel(fast[sub], truth) <= TOL[precision.value], precision
+        exact = il.run_nested_improved(store, queries[sub], cfg=il.ExecConfig(mode="exact"))
+        assert np.array_equal(exact, oracle.nested_improved(store, queries[sub])), precision
