@@ -110,6 +110,13 @@ int launch_tiled(Launch &L) {
         if (jq == 7) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 0, 7>;
         if (jq == 6) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 0, 6>;
       }
+      if constexpr (sizeof(T) == 4 && MODE == FAST && !P2 && Q % 2 == 0) {
+        // integer p = 1, 3, 4: one MUFU per pair (rsqrt / rcp powers) instead of lg2 + ex2
+        const int jq = make_scal<T>(L).jq;
+        if (jq == 2) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 0, 2>;
+        if (jq == 6) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 0, 6>;
+        if (jq == 8) kern = k_tiled<K, T, MODE, P2, EPS, Q, TILE, 0, 8>;
+      }
       const int smem_max = (C::NC_MAX / 32) * RING;
       int occ = 0;
       if (int rc = kernel_occupancy((const void *)kern, L.dev, C::NC_MAX, smem_max, &occ)) return rc;

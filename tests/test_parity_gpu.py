@@ -442,3 +442,22 @@ def test_split_reduce_persistent_clusters(il):
         assert rel(fast[sub], truth) <= TOL[precision.value], precision
         exact = il.run_nested_improved(store, queries[sub], cfg=il.ExecConfig(mode="exact"))
         assert np.array_equal(exact, oracle.nested_improved(store, queries[sub])), precision
+
+
+@pytest.mark.parametrize("p", [1.0, 3.0, 4.0, 1.5])
+def test_fast_fp32_integer_p(il, p):
+    """FAST fp32 integer p compiles to one MUFU per pair (rsqrt^p for odd p,
+    rcp^(p/2) for even p; p = 1.5 keeps lg2/ex2): within 1e-5 of the fp64
+    truth for tiled, split-reduce and naive, with a coincident query fixed up
+    exactly."""
+    rng = np.random.default_rng(83)
+    data = random_records(rng, 40_000)
+    queries = random_queries(rng, 3000)
+    queries[11] = data[5, :2]
+    for kind in (il.LayoutKind.AoaS, il.LayoutKind.SoA):
+        store = il.build(data, kind, il.Precision.single)
+        truth = oracle.truth(store, queries, p)
+        for s in ("tiled", "nested_improved", "naive"):
+            got = il.STRATEGIES[s](store, queries, il.Params(p), cfg=il.ExecConfig(mode="fast"))
+            assert got[11] == store.to_arrays()[2][5], (kind, s)
+            assert rel(got, truth) <= 1e-5, (kind, p, s)
