@@ -361,6 +361,16 @@ def run_ours(args):
     if prec == "double":
         roof["peak_source"] = (f"FP64 pipe: {sms} SMs x 64 DP lanes/clk x run clock / {dp_ops} DP ops per pair "
                                "(DFMA measured 62/clk/SM in tools/microbench.cu)")
+        # BASELINE.md §3 states the fp64 rooflines with the textbook arithmetic:
+        # 10 DP instr/pair for p = 2, 6 + D_pow for general p, D_pow = 47 DP
+        # instructions on the fast path of CUDA 12.9 exp2(wexp * log2(d2)) in
+        # double (SASS of a probe kernel: 28 for log2, 19 for the multiply and
+        # exp2).  The kernel's reformulated arithmetic needs fewer.
+        base_ops = 10 if p == 2.0 else 6 + 47
+        base_peak = sms * 64 * mhz * 1e6 / base_ops / 1e9
+        roof["baseline_definition"] = {"dp_ops_per_pair": base_ops, "peak": base_peak, "frac": achieved / base_peak,
+                                       "note": "BASELINE.md section 3 roofline; peak/frac above use the kernel's "
+                                               f"own {dp_ops} DP ops per pair"}
     elif p == 2.0 and args.mode == "fast" and variant == "tiled":
         # The BASELINE roofline charges one MUFU reciprocal per pair.  k_tiled
         # computes one of its four packed query pairs with a shared reciprocal
