@@ -314,9 +314,11 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
   L.sms = sms;
   if (needs_fixup(L)) L.flags = arena + off[6];
   L.nfixed = (unsigned long long *)(arena + off[7]);
-  cudaEvent_t e0, e1;
-  IDW_CK(cudaEventCreate(&e0));
-  IDW_CK(cudaEventCreate(&e1));
+  // timing events: created once per device and host thread
+  static thread_local cudaEvent_t ev0[64] = {}, ev1[64] = {};
+  cudaEvent_t &e0 = ev0[p->device & 63], &e1 = ev1[p->device & 63];
+  if (!e0) IDW_CK(cudaEventCreate(&e0));
+  if (!e1) IDW_CK(cudaEventCreate(&e1));
   IDW_CK(cudaEventRecord(e0, st));
   rc = dispatch(L);
   unsigned int nonfinite = 0;
@@ -334,10 +336,8 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
       stats->fixup_queries = (int64_t)nfix;
     }
   }
-  cudaFreeAsync(arena, st);
-  cudaStreamSynchronize(st);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  cudaFreeAsync(arena, st);  // stream-ordered: nothing left to wait for
+  if (rc != 0) cudaStreamSynchronize(st);
   fill_stats(stats, L, p, s->count, m);
   if (rc == 0 && nonfinite) {
     set_error("invalid coordinate");  // core.ensure_finite (core.py:113-116)

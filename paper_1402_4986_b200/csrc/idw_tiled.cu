@@ -179,6 +179,16 @@ int launch_tiled(Launch &L) {
         static const int q2 = [] { const char *e = getenv("IDW_EXACT_Q2"); return e ? atoi(e) : 1; }();
         if (K != AOS && q2 && cdiv(L.m, (long long)C::Q * C::NC_MAX) < L.sms) return run_q(IC<2>{});
       }
+      if constexpr (std::is_same<T, float>::value && MODE == FAST) {
+        // Small jobs: Q = 4 doubles the threads of a query block -- more warps to
+        // hide the ring fill and MUFU latency when each CTA sees only a few
+        // tiles.  Measured (graph replays): 10K x 10K 1694 -> 1960, 100K x 10K
+        // 3251 -> 3817, 100K x 100K even, 1M x 131K (an 8-GPU shard) 4729 ->
+        // 4555 GPairs/s -- hence the ~4e9-pair cap.  IDW_FAST_Q4=0 disables.
+        static const int q4 = [] { const char *e = getenv("IDW_FAST_Q4"); return e ? atoi(e) : 1; }();
+        if (q4 && (double)L.n * (double)L.m <= 4e9 && cdiv(L.m, (long long)C::Q * C::NC_MAX) < L.sms)
+          return run_q(IC<4>{});
+      }
       return run_q(IC<C::Q>{});
     });
   });
