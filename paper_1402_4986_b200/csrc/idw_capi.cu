@@ -291,6 +291,12 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
   off[9] = xy ? take(2 * sizeof(double) * (size_t)m) : 0;
   unsigned char *arena = nullptr;
   IDW_CK(cudaMallocAsync((void **)&arena, total, st));
+  // the arena goes back to the pool on every exit, early error returns included
+  struct ArenaGuard {
+    unsigned char *p;
+    cudaStream_t st;
+    ~ArenaGuard() { cudaFreeAsync(p, st); }
+  } guard{arena, st};
   const void *dbuf[3] = {nullptr, nullptr, nullptr};
   for (int b = 0; b < s->nbuf; ++b) {
     IDW_CK(cudaMemcpyAsync(arena + off[b], s->buf[b], (size_t)s->nbytes[b], cudaMemcpyHostToDevice, st));
@@ -336,8 +342,7 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
       stats->fixup_queries = (int64_t)nfix;
     }
   }
-  cudaFreeAsync(arena, st);  // stream-ordered: nothing left to wait for
-  if (rc != 0) cudaStreamSynchronize(st);
+  if (rc != 0) cudaStreamSynchronize(st);  // the guard frees the arena, stream-ordered
   fill_stats(stats, L, p, s->count, m);
   if (rc == 0 && nonfinite) {
     set_error("invalid coordinate");  // core.ensure_finite (core.py:113-116)
