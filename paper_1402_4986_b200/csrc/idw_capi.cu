@@ -247,9 +247,12 @@ int idw_run_device(const idw_store *s, const void *qx, const void *qy, int64_t m
   L.dev = p->device;
   L.sms = sms;
   unsigned char *flags = nullptr;
+  StreamFree free_flags;
   if (needs_fixup(L)) {
     IDW_CK(cudaMallocAsync((void **)&flags, (size_t)m, L.st));
     L.flags = flags;
+    free_flags.p = flags;
+    free_flags.st = L.st;
   }
   EvSet &ev = g_ev[p->device];
   if (!ev.a) {
@@ -259,7 +262,6 @@ int idw_run_device(const idw_store *s, const void *qx, const void *qy, int64_t m
   }
   rc = dispatch(L, &ev);
   g_last_dev = rc == 0 ? p->device : -1;
-  if (flags) cudaFreeAsync(flags, L.st);
   fill_stats(stats, L, p, s->count, m);
   return rc;
 }

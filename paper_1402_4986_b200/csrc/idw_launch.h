@@ -50,6 +50,18 @@ void set_error(const std::string &msg);
     }                                                                                   \
   } while (0)
 
+// Stream-ordered scratch released on scope exit (early error returns included).
+struct StreamFree {
+  void *p = nullptr;
+  cudaStream_t st = nullptr;
+  StreamFree() = default;
+  StreamFree(const StreamFree &) = delete;
+  StreamFree &operator=(const StreamFree &) = delete;
+  ~StreamFree() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
 template <int V>
 using IC = std::integral_constant<int, V>;
 template <bool V>

@@ -130,12 +130,15 @@ int launch_tiled(Launch &L) {
       SplitOut<T> so{nullptr, nullptr, nullptr, nullptr, nullptr};
       void *ws = nullptr;
       float4 *dbox = nullptr;
+      StreamFree free_box, free_ws;  // scratch goes back to the pool on every exit
       using AccT = typename AccSelNT<T, MODE, P2, EPS, Q>::type;
       constexpr bool EXACT_FR = std::is_same<AccT, AccExactScr2<Q>>::value ||
                                std::is_same<AccT, AccExactScr<double, true, Q>>::value;
       if (prod_used || EXACT_FR) {  // data box for the fast-path guards
         const int nb = (int)std::min<long long>(cdiv(L.n, 256), (long long)L.sms * 4);
         IDW_CK(cudaMallocAsync((void **)&dbox, sizeof(float4) * (nb + 1), L.st));
+        free_box.p = dbox;
+        free_box.st = L.st;
         k_bbox_partial<K, T><<<nb, 256, 0, L.st>>>(L.g, L.n, dbox + 1);
         IDW_CK_LAUNCH();
         k_bbox_final<<<1, 32, 0, L.st>>>(dbox + 1, nb, dbox);
@@ -145,6 +148,8 @@ int launch_tiled(Launch &L) {
       if (sh.splits > 1) {
         const size_t per = (size_t)sh.splits * (size_t)L.m;
         IDW_CK(cudaMallocAsync(&ws, per * (4 * sizeof(T) + 1), L.st));
+        free_ws.p = ws;
+        free_ws.st = L.st;
         T *base = (T *)ws;
         so.shi = base;
         so.slo = base + per;
@@ -157,7 +162,6 @@ int launch_tiled(Launch &L) {
                                      make_scal<T>(L), (T *)L.out, L.flags, so, dbox);
       IDW_CK_LAUNCH();
       ++L.launches;
-      if (dbox) IDW_CK(cudaFreeAsync(dbox, L.st));
       if (sh.splits > 1) {
         if constexpr (MODE == FAST) {
           k_combine<T><<<(unsigned)cdiv(L.m, 256), 256, 0, L.st>>>(L.m, (int)sh.splits, so, (T)L.eps_flag,
@@ -165,7 +169,6 @@ int launch_tiled(Launch &L) {
           IDW_CK_LAUNCH();
           ++L.launches;
         }
-        IDW_CK(cudaFreeAsync(ws, L.st));
       }
       return 0;
       };
