@@ -461,3 +461,25 @@ def test_fast_fp32_integer_p(il, p):
             got = il.STRATEGIES[s](store, queries, il.Params(p), cfg=il.ExecConfig(mode="fast"))
             assert got[11] == store.to_arrays()[2][5], (kind, s)
             assert rel(got, truth) <= 1e-5, (kind, p, s)
+
+
+def test_exact_split_reduce_subnormal_d2_bitwise(il):
+    """Screened EXACT split-reduce in fp32 runs packed query pairs with
+    __frcp_rn's fast path inline; a subnormal d2 (which that path flushes)
+    leaves the query flagged, and k_fixup recomputes it in K3's own order
+    (G strided lanes + adjacent-pair tree).  Queries a subnormal distance
+    (d2 ~ 2^-127.5, 1/d2 still finite) from a data point at the origin must
+    come out bit-identical to the reference's nested_improved."""
+    rng = np.random.default_rng(89)
+    data = random_records(rng, 3000, 0.0, 1.0)
+    data[:, :2] = 0.1 + 0.9 * data[:, :2]
+    data[7] = (0.0, 0.0, 0.37)
+    deltas = [2.0 ** -63.2, 2.0 ** -63.5, 2.0 ** -63.8, 2.0 ** -63.95]
+    queries = np.vstack([np.array([[d, 0.0] for d in deltas] + [[0.0, d] for d in deltas]),
+                         random_queries(rng, 200)])
+    store = il.build(data, il.LayoutKind.SoA, il.Precision.single)
+    for G in (1024, 256, 64):
+        ref = oracle.nested_improved(store, queries, group=G)
+        assert np.all(np.isfinite(ref[:8]))
+        got = il.run_nested_improved(store, queries, cfg=il.ExecConfig(mode="exact", group_size=G))
+        assert np.array_equal(got.view(np.uint8), ref.view(np.uint8)), G
