@@ -483,3 +483,23 @@ def test_exact_split_reduce_subnormal_d2_bitwise(il):
         assert np.all(np.isfinite(ref[:8]))
         got = il.run_nested_improved(store, queries, cfg=il.ExecConfig(mode="exact", group_size=G))
         assert np.array_equal(got.view(np.uint8), ref.view(np.uint8)), G
+
+
+def test_exact_split_reduce_subnormal_d2_bitwise_fp64(il):
+    """fp64 counterpart: the inline __drcp_rn path seeds inf for a subnormal
+    d2 (~2^-1023.5, 1/d2 still finite); the query is recomputed in K3's order
+    by k_fixup and must match the reference's nested_improved bitwise."""
+    rng = np.random.default_rng(97)
+    data = random_records(rng, 3000, 0.0, 1.0)
+    data[:, :2] = 0.1 + 0.9 * data[:, :2]
+    data[7] = (0.0, 0.0, 0.37)
+    deltas = [2.0 ** -511.2, 2.0 ** -511.6, 2.0 ** -511.9]
+    queries = np.vstack([np.array([[d, 0.0] for d in deltas] + [[0.0, d] for d in deltas]),
+                         random_queries(rng, 200)])
+    for kind in (il.LayoutKind.SoA, il.LayoutKind.Hybrid):
+        store = il.build(data, kind, il.Precision.double)
+        for G in (1024, 128):
+            ref = oracle.nested_improved(store, queries, group=G)
+            assert np.all(np.isfinite(ref[:6]))
+            got = il.run_nested_improved(store, queries, cfg=il.ExecConfig(mode="exact", group_size=G))
+            assert np.array_equal(got.view(np.uint8), ref.view(np.uint8)), (kind, G)
