@@ -483,6 +483,11 @@ def test_exact_split_reduce_subnormal_d2_bitwise(il):
         assert np.all(np.isfinite(ref[:8]))
         got = il.run_nested_improved(store, queries, cfg=il.ExecConfig(mode="exact", group_size=G))
         assert np.array_equal(got.view(np.uint8), ref.view(np.uint8)), G
+    # the strict-order strategies take the same inline path (sequential recompute)
+    ref = oracle.predict(store, queries)
+    for s in ("naive", "tiled"):
+        got = il.STRATEGIES[s](store, queries, cfg=il.ExecConfig(mode="exact"))
+        assert np.array_equal(got.view(np.uint8), ref.view(np.uint8)), s
 
 
 def test_exact_split_reduce_subnormal_d2_bitwise_fp64(il):
