@@ -85,3 +85,16 @@ def test_no_cpu_fallback():
 
     with pytest.raises(_capi.NativeError):
         il.run_tiled(st, [(0.5, 0.5)])
+
+
+def test_header_codes_match_python_tables():
+    """enum values of include/idw_b200.h == the codes the ctypes layer sends."""
+    text = HEADER.read_text()
+    enums = dict((k, int(v)) for k, v in re.findall(r"\b(IDW_[A-Z_0-9]+)\s*=\s*(-?\d+)", text))
+    assert {k: enums[f"IDW_{k.upper()}"] for k in _capi.KIND_CODES} == _capi.KIND_CODES
+    assert enums["IDW_SINGLE"] == _capi.PRECISION_CODES["single"]
+    assert enums["IDW_DOUBLE"] == _capi.PRECISION_CODES["double"]
+    for name, code in _capi.VARIANT_CODES.items():
+        assert enums[f"IDW_{name.upper()}"] == code
+    assert enums["IDW_EXACT"] == _capi.MODE_CODES["exact"] and enums["IDW_FAST"] == _capi.MODE_CODES["fast"]
+    assert enums["IDW_E_NONFINITE"] == _capi.E_NONFINITE
