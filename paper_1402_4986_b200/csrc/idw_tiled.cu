@@ -135,15 +135,9 @@ int launch_tiled(Launch &L) {
       constexpr bool EXACT_FR = std::is_same<AccT, AccExactScr2<Q>>::value ||
                                std::is_same<AccT, AccExactScr<double, true, Q>>::value;
       if (prod_used || EXACT_FR) {  // data box for the fast-path guards
-        const int nb = (int)std::min<long long>(cdiv(L.n, 256), (long long)L.sms * 4);
-        IDW_CK(cudaMallocAsync((void **)&dbox, sizeof(float4) * (nb + 1), L.st));
+        if (int rc = launch_bbox<K, T>(L, &dbox)) return rc;
         free_box.p = dbox;
         free_box.st = L.st;
-        k_bbox_partial<K, T><<<nb, 256, 0, L.st>>>(L.g, L.n, dbox + 1);
-        IDW_CK_LAUNCH();
-        k_bbox_final<<<1, 32, 0, L.st>>>(dbox + 1, nb, dbox);
-        IDW_CK_LAUNCH();
-        L.launches += 2;
       }
       if (sh.splits > 1) {
         const size_t per = (size_t)sh.splits * (size_t)L.m;
