@@ -1,0 +1,8 @@
+#!/bin/bash
+OUT=gpurun_out/sanitizer
+mkdir -p $OUT
+for tool in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $tool --target-processes all --print-limit 20 \
+      python tools/sanitize_target.py > $OUT/$tool.log 2>&1
+  echo "rc=$?" >> $OUT/$tool.log
+done
