@@ -174,8 +174,10 @@ def run_reference(args):
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle
 
+    import refinputs  # oracle/: inputs built without the product package
+
     n, m, layout, prec, variant, p, desc = CONFIGS[args.config]
-    store, queries = make_inputs(args.config)
+    store, queries = refinputs.bench_inputs(n, m, layout, prec)
     threads = oracle.max_threads()
     # size one step for ~6 s of CPU work
     m0 = threads * 16
@@ -205,6 +207,15 @@ def run_reference(args):
                                    f"{threads} pthreads, 256-query blocks)"},
         "e2e": {"value": value, "unit": "GPairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    # the arm must not have touched the product (its package or its library)
+    imported = sorted(k for k in sys.modules if k.startswith("paper_1402_4986_b200"))
+    try:
+        mapped = "libidw_b200" in Path("/proc/self/maps").read_text()
+    except OSError:
+        mapped = False
+    if imported or mapped:
+        raise SystemExit(f"reference arm touched the product: modules={imported} libidw_b200 mapped={mapped}")
+    line["product_loaded"] = False
     print(json.dumps(line), flush=True)
     return 0
 

@@ -39,3 +39,19 @@ def test_reference_arm_nonzero_rank_is_silent():
              {"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == ""
+
+
+def test_reference_arm_never_loads_the_product():
+    """the CPU arm runs the reference algorithm only --
+    neither the product package nor libidw_b200.so may be loaded."""
+    r = _run(["--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "1"])
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["product_loaded"] is False
+    # and in-process: the oracle-side input builder alone imports no product module
+    code = ("import sys; sys.path.insert(0, 'oracle'); import refinputs, oracle; "
+            "s, q = refinputs.bench_inputs(4096, 64, 'aoas', 'single'); oracle.predict(s, q); "
+            "assert not [k for k in sys.modules if k.startswith('paper_1402_4986_b200')]; "
+            "assert 'libidw_b200' not in open('/proc/self/maps').read()")
+    r2 = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=120)
+    assert r2.returncode == 0, r2.stderr

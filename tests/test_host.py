@@ -153,3 +153,22 @@ def test_strategy_validation_before_native_call():
     assert strategies.strategy_tolerance(Precision.single, 256) == 1e-4
     assert strategies.strategy_tolerance(Precision.single, 257) == 1e-3
     assert set(il.STRATEGIES) == {"naive", "tiled", "nested_original", "nested_improved"}
+
+
+def test_oracle_side_inputs_match_product(golden):
+    """oracle/refinputs.py (used by bench's reference arm, which must not
+    import the product) builds the same cloud and the same component values."""
+    import refinputs
+
+    x, y, z = refinputs.cloud(10 * 1024, 7)
+    assert float(np.sum(x) + np.sum(y) + np.sum(z)) == golden["gen/cloud10k_seed7_sum"][0]
+    assert refinputs.query_seed(0) == il.query_seed(0)
+    px, py, pz = il.generate_cloud_arrays(5000, 3)
+    for kind, precision in legal_pairs():
+        ours = LayoutStore.from_arrays(px, py, pz, kind, precision)
+        ref = refinputs.OracleStore(px, py, pz, kind.value, precision.value)
+        for a, b in zip(ours.component_views(), ref.component_views()):
+            assert a.dtype == b.dtype and np.array_equal(a, b), (kind, precision)
+        if kind.value in ("soa", "aos", "aoas"):
+            assert b"".join(bytes(np.ascontiguousarray(b)) for b in ref.buffers) == ours.to_bytes()[-sum(
+                b.nbytes for b in ours.buffers):], (kind, precision)
