@@ -70,6 +70,7 @@ def parse_args():
     ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl")
     ap.add_argument("--device-override", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     return ap.parse_args()
 
 
@@ -478,6 +479,36 @@ def run_ours(args):
                "sample": f"{n} data x {msub} queries ({dt:.1f} s), oracle/idw_oracle.c predict_block "
                          f"(reference kernels.py:34-67 restated in C), {threads} pthreads"}
 
+    # ---- parity of the timed output (rank 0's shard; outside the timed region).
+    # Each prediction depends only on its query and all n points
+    # (kernels.py:42-67), so a strided query subsample checks it exactly.
+    parity = None
+    if rank == 0 and not args.no_parity:
+        import numpy as np
+
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle
+
+        nchk = 1024 if n <= (1 << 20) else 256
+        idx = np.unique(np.linspace(0, hi - lo - 1, nchk).astype(np.int64))
+        got = out_l.cpu().numpy()[idx]
+        sub = queries[lo:hi][idx]
+        if args.mode == "fast":
+            ref = oracle.truth(store, sub, p)
+            kind = "oracle.truth (fp64 double-double on the run-precision inputs)"
+        elif variant == "nested_improved":
+            ref = oracle.nested_improved_mt(store, sub, p)
+            kind = "oracle.nested_improved (reference nested_improved_block restated, G=1024)"
+        else:
+            ref = oracle.predict_mt(store, sub, p)
+            kind = "oracle.predict (reference predict_block restated)"
+        a, b = got.astype(np.float64), np.asarray(ref, np.float64)
+        err = float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
+        tol = 1e-5 if prec == "single" else 1e-12
+        parity = {"max_rel_err": err, "queries_checked": int(idx.size), "oracle": kind,
+                  "tolerance": tol, "pass": bool(err <= tol),
+                  "bitwise": bool(np.array_equal(got, np.asarray(ref, got.dtype))) if args.mode == "exact" else None}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GPairs/s", "n_gpus": world, "steps": args.steps,
@@ -490,7 +521,7 @@ def run_ours(args):
                        "parallelism": f"query-shard x{world} (data broadcast + gather per step)",
                        "l2": "flushed between steps (256 MiB write, outside the per-step event pairs); "
                              "inputs resident in HBM"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "parity": parity,
             "gpu_launches": launches[0],
             "mufu_probe": {"rcp_per_s": probe_rate},
         }

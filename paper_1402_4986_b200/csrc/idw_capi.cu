@@ -58,8 +58,13 @@ static int nbuf_of(int kind) {
   return kind == IDW_SOA ? 3 : (kind == IDW_AOS || kind == IDW_AOAS) ? 1 : 2;
 }
 
+// device_ptrs: the store buffers are read in place by the kernels, so their
+// alignment matters (host buffers are staged into a 256-byte-aligned arena).
+// K2 stages tiles with cp.async.bulk, which needs a 16-byte-aligned source for
+// every layout; the other variants need 16 bytes where they issue vector
+// loads (every layout but AoS, whose 12/24-byte records take scalar loads).
 static int validate(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p,
-                    const void *out) {
+                    const void *out, bool device_ptrs) {
   if (!s || !p) return set_error("null store or params"), IDW_E_ARG;
   if (s->kind < 0 || s->kind > 4) return set_error("unknown layout kind"), IDW_E_ARG;
   if (s->precision != IDW_SINGLE && s->precision != IDW_DOUBLE) return set_error("unknown precision"), IDW_E_ARG;
@@ -71,9 +76,11 @@ static int validate(const idw_store *s, const void *qx, const void *qy, int64_t 
     if (!s->buf[b]) return set_error("null store buffer"), IDW_E_ARG;
     const int64_t need = s->count * (int64_t)bytes_per_point(s->kind, s->precision, b);
     if (s->nbytes[b] < need) return set_error("store buffer shorter than its shape"), IDW_E_ARG;
-    const int align = s->kind == IDW_AOS ? (s->precision == IDW_SINGLE ? 4 : 8) : 16;
-    if (((uintptr_t)s->buf[b]) % 16 != 0 && align == 16)
-      return set_error("store buffer not 16-byte aligned"), IDW_E_ARG;
+    if (device_ptrs && p) {
+      const int align = (s->kind == IDW_AOS && p->variant != IDW_TILED) ? (s->precision == IDW_SINGLE ? 4 : 8) : 16;
+      if (((uintptr_t)s->buf[b]) % align != 0)
+        return set_error("device store buffer not " + std::to_string(align) + "-byte aligned"), IDW_E_ARG;
+    }
   }
   if (m < 0) return set_error("negative query count"), IDW_E_ARG;
   if (m > 0 && (!qx || !qy || !out)) return set_error("null query or output pointer"), IDW_E_ARG;
@@ -235,7 +242,7 @@ const char *idw_last_error(void) { return g_err.c_str(); }
 int idw_run_device(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p, void *out,
                    void *stream, idw_stats *stats) {
   g_err.clear();
-  int rc = validate(s, qx, qy, m, p, out);
+  int rc = validate(s, qx, qy, m, p, out, true);
   if (rc) return rc;
   if (m == 0) return 0;
   cudaStream_t dst;
@@ -368,7 +375,7 @@ int idw_plan_create(const idw_store *s, const void *qx, const void *qy, int64_t 
   g_err.clear();
   if (!plan) return set_error("null plan pointer"), IDW_E_ARG;
   *plan = nullptr;
-  int rc = validate(s, qx, qy, m, p, out);
+  int rc = validate(s, qx, qy, m, p, out, true);
   if (rc) return rc;
   if (m == 0) return set_error("a plan needs at least one query"), IDW_E_ARG;
   cudaStream_t dst;
@@ -455,7 +462,7 @@ void idw_plan_destroy(idw_plan *pl) {
 int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p, void *out,
             idw_stats *stats) {
   g_err.clear();
-  int rc = validate(s, qx, qy, m, p, out);
+  int rc = validate(s, qx, qy, m, p, out, false);
   if (rc) return rc;
   if (m == 0) return 0;
   return run_host(s, qx, qy, nullptr, m, p, out, stats);
@@ -463,7 +470,7 @@ int idw_run(const idw_store *s, const void *qx, const void *qy, int64_t m, const
 
 int idw_run_xy(const idw_store *s, const double *xy, int64_t m, const idw_params *p, void *out, idw_stats *stats) {
   g_err.clear();
-  int rc = validate(s, xy, xy, m, p, out);
+  int rc = validate(s, xy, xy, m, p, out, false);
   if (rc) return rc;
   if (m == 0) return 0;
   return run_host(s, nullptr, nullptr, xy, m, p, out, stats);
