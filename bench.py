@@ -361,7 +361,7 @@ def run_ours(args):
         "unit": "GPairs/s",
         "frac": achieved / peak,
         "traffic": None,
-        "kernel": "k_tiled" if variant == "tiled" else "k_nested",
+        "kernel": ("k_tiled_chunks" if args.mode == "fast" else "k_tiled") if variant == "tiled" else "k_nested",
         "kernel_ms": kmain,
         "fixup_ms": kfix,
         "peak_source": "measured: idw_mufu_peak probe (independent rcp.approx chains on all "
@@ -384,7 +384,7 @@ def run_ours(args):
                                        "note": "BASELINE.md section 3 roofline; peak/frac above use the kernel's "
                                                f"own {dp_ops} DP ops per pair"}
     elif p == 2.0 and args.mode == "fast" and variant == "tiled":
-        # The BASELINE roofline charges one MUFU reciprocal per pair.  k_tiled
+        # The BASELINE roofline charges one MUFU reciprocal per pair.  k_tiled_chunks
         # computes one of its four packed query pairs with a shared reciprocal
         # (r = 1/(a*b), 1/a = b*r, 1/b = a*r), i.e. 7 MUFU per 8 pairs, so it
         # can pass that line; its own MUFU ceiling is peak * 8/7 (and the
@@ -393,7 +393,7 @@ def run_ours(args):
         mix_peak = peak * 8.0 / 7.0
         roof["kernel_mix_bound"] = {
             "mufu_per_pair": 7.0 / 8.0, "peak": mix_peak, "frac": achieved / mix_peak,
-            "note": "MUFU ceiling of k_tiled's own instruction mix (shared reciprocal for 1 of 4 query pairs)"}
+            "note": "MUFU ceiling of k_tiled_chunks' own instruction mix (shared reciprocal for 1 of 4 query pairs)"}
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
     # Algorithmic (compulsory) bytes of one launch: the store, the cast query
     # coordinates in, the predictions out -- n*S_rec + 3*m_shard*e.
@@ -401,14 +401,16 @@ def run_ours(args):
     srec = {"soa": 3 * e_sz, "aos": 3 * e_sz, "aoas": 4 * e_sz, "soaos": 32, "hybrid": 24}[layout]
     roof["algorithmic_bytes"] = float(n * srec + 3 * (hi - lo) * e_sz)
     # DRAM traffic of the dominant kernel from the committed ncu --set full
-    # capture of the same configuration (tools/gpu_round_final.sh)
-    caps = {"c1": "prof_c1", "c2": "prof_c2", "c3": "prof_c3_tiled", "c5": "prof_c5"}
-    prof = ROOT / "profiles" / "r1" / f"{caps.get(args.config, '-')}.raw.csv"
-    if prof.exists() and args.mode == "fast" and world == 1:
+    # capture of the same configuration (profiles/r2, tools/gpu_r2_profiles.sh)
+    caps = {"c1": "prof_c1", "c2": "prof_c2", "c3": "prof_c3", "c5": "prof_c5"}
+    prof = ROOT / "profiles" / "r2" / f"{caps.get(args.config, '-')}.raw.csv"
+    if prof.exists() and args.mode == "fast" and world == 1 and variant == "tiled":
         import csv
 
         rows = list(csv.reader(open(prof)))
-        d = dict(zip(rows[0], rows[2]))
+        kcol = rows[0].index("Kernel Name")
+        row = next((r for r in rows[2:] if "k_tiled_chunks" in r[kcol]), None)
+        d = dict(zip(rows[0], row)) if row else {}
         u = dict(zip(rows[0], rows[1]))
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         try:
@@ -417,14 +419,15 @@ def run_ours(args):
             roof["traffic"] = rd + wr
             roof["traffic_read"] = rd
             roof["traffic_write"] = wr
-            roof["traffic_source"] = f"{prof.relative_to(ROOT)} (ncu --set full, one k_tiled launch, same config)"
-            roof["traffic_note"] = ("writes above the algorithmic bytes are the per-split partial sums of the "
-                                    "data-split grid (splits x m x 17 B, folded by k_combine), not re-reads")
+            roof["traffic_source"] = (f"{prof.relative_to(ROOT)} (ncu --set full, one k_tiled_chunks launch, "
+                                      "same config)")
+            roof["traffic_note"] = ("chunk partials live in an L2-resident ring of group slots (recycled after "
+                                    "each group's fold), so DRAM sees the store, the queries and the outputs")
         except (KeyError, ValueError):
             pass
 
     # ---- e2e through the public drop-in API (host buffers, blocking)
-    e2e = None
+    e2e = e2e_pageable = None
     if not args.no_e2e:
         fn = il.STRATEGIES[variant]
         local_store = store
@@ -465,6 +468,24 @@ def run_ours(args):
                "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": int(d2h_all),
                "api": f"paper_1402_4986_b200.{fn.__name__}(LayoutStore[pinned host], queries[host f64], "
                       f"Params(p={p}), ExecConfig(mode='{args.mode}'))"}
+        # the same through the caller's plain (pageable) numpy buffers: the
+        # reference's own run_* callers hold ordinary arrays
+        pstore = il.LayoutStore(local_store.kind, local_store.precision, n,
+                                [np.array(b, copy=True) for b in local_store.buffers], local_store.shapes)
+        fn(pstore, hq, params, cfg)
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res = fn(pstore, hq, params, cfg)
+        t_pg = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([t_pg], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_pg = float(t.item())
+        e2e_pageable = {"value": total_pairs * args.steps / t_pg / 1e9, "unit": "GPairs/s",
+                        "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": int(d2h_all),
+                        "api": e2e["api"].replace("pinned host", "pageable host")}
         del res
 
     # ---- CPU baseline (rank 0, N = 1 only)
@@ -521,7 +542,8 @@ def run_ours(args):
                        "parallelism": f"query-shard x{world} (data broadcast + gather per step)",
                        "l2": "flushed between steps (256 MiB write, outside the per-step event pairs); "
                              "inputs resident in HBM"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "parity": parity,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_pageable": e2e_pageable,
+            "clocks": clocks, "parity": parity,
             "gpu_launches": launches[0],
             "mufu_probe": {"rcp_per_s": probe_rate},
         }

@@ -112,7 +112,17 @@ int kernel_occupancy(const void *kern, int dev, int threads, int smem, int *occ)
     auto it = cache.find(key);
     if (it != cache.end()) return *occ = it->second, 0;
   }
-  if (smem > 48 * 1024) IDW_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  {
+    // the attribute is a per-kernel ceiling: only ever raise it, so a launch
+    // shaped for more shared memory stays valid after a smaller query
+    static std::map<std::pair<const void *, int>, int> ceiling;
+    std::lock_guard<std::mutex> lk(mu);
+    int &c = ceiling[{kern, dev}];
+    if (smem > 48 * 1024 && smem > c) {
+      IDW_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      c = smem;
+    }
+  }
   int o = 0;
   IDW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem));
   std::lock_guard<std::mutex> lk(mu);

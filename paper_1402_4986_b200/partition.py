@@ -11,8 +11,11 @@ all data (kernels.py:42-67), so the B200 design shards QUERIES:
   3. the per-rank predictions are gathered to the root in rank order.
 
 There is no reduction, so every query keeps its single-device summation
-order and results are bit-identical for any world size.  Shards are sized in
-whole ``align``-query units so that the per-GPU kernel grids stay balanced.
+order and results are bit-identical for any world size, in both modes: EXACT
+sums in the reference's strict order, and FAST's summation chunks depend on n
+alone while its query groups (32*Q consecutive queries) stay whole inside
+``align``-query shards (align = 256, a multiple of every group size;
+tests/test_determinism_gpu.py checks 1 vs 2/4/8 shards bitwise at C3).
 """
 
 from __future__ import annotations

@@ -16,10 +16,16 @@ underneath is one blocking call into libidw_b200 per strategy call:
             "fast"  -- MUFU/FMA/f32x2 arithmetic, blocked compensated sums,
             exact fix-up of coincident queries; held to the tolerance table.
     device  CUDA ordinal (default env IDW_DEVICE or 0)
-    splits  FAST tiled data splits (0 = auto)
+    splits  FAST tiled summation chunks (0 = auto: a function of n alone).
+            A nonzero value fixes the chunk count instead; it is part of the
+            summation order, so it changes the FAST bits (still within the
+            tolerance) -- nothing else the caller sets does.
 
 ``parallel_width`` is accepted and validated for compatibility; GPU results do
-not depend on it (nor on any other scheduling knob).
+not depend on it.  ``tile_size`` is validated and kept for the read counters
+(tiled: ceil(m/G)*n per component, as the reference counts them) but the GPU
+tiles are fixed by the kernels (fp32 256 points, fp64 128): K2's arithmetic
+does not change with it, so results never depend on it.
 """
 
 from __future__ import annotations

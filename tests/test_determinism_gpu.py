@@ -1,0 +1,122 @@
+"""Results independent of how the queries are cut up (GPU).
+
+The reference pins its outputs bit-identical across worker counts
+(test_acceptance.py:181-203, test_strategies.py:211-223): its query blocks
+depend only on the workload (strategies.py:15-21,137-138) and every query is
+summed in one fixed order.  The B200 analogue: a query's bits must not depend
+on m, on the other queries of the call, or on how many devices share the job.
+
+  EXACT   strict reference order -> trivially invariant (checked anyway).
+  FAST    tiled: the summation chunks are a function of n alone and queries
+          sit in fixed 32*Q-query groups, so any split of the query array at
+          group-aligned boundaries (partition.shard_bounds with align=256)
+          reproduces the single-call bits; split-reduce and naive have no
+          m-dependent state at all.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+ALIGN = 256  # partition.py's shard alignment (a multiple of every K2/K3 query group)
+
+
+@pytest.fixture(scope="module")
+def il():
+    import paper_1402_4986_b200 as pkg
+
+    if pkg._capi.device_count() < 1:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+    return pkg
+
+
+def cloud(il, n, m, kind="aoas", prec="single"):
+    x, y, z = il.generate_cloud_arrays(n, 0)
+    qx, qy, _ = il.generate_cloud_arrays(m, il.query_seed(0))
+    store = il.LayoutStore.from_arrays(x, y, z, il.LayoutKind(kind), il.Precision(prec))
+    return store, np.column_stack([qx, qy])
+
+
+def sharded(il, fn, store, queries, world, params, cfg):
+    from paper_1402_4986_b200.partition import shard_bounds
+
+    parts = []
+    for r in range(world):
+        lo, hi = shard_bounds(len(queries), world, r, ALIGN)
+        parts.append(fn(store, queries[lo:hi], params, cfg))
+    return np.concatenate(parts)
+
+
+def test_fast_tiled_c3_full_equals_eight_shards(il):
+    """C3 (1M x 1M, fp32 AoaS, FAST tiled): one call == 8 shard calls, bitwise;
+    also == 2 and 4 shards, and a group-aligned prefix of the queries."""
+    n = m = 1 << 20
+    store, queries = cloud(il, n, m)
+    cfg = il.ExecConfig(mode="fast")
+    full = il.run_tiled(store, queries, il.Params(), cfg)
+    for world in (8, 2, 4):
+        got = sharded(il, il.run_tiled, store, queries, world, il.Params(), cfg)
+        assert np.array_equal(got, full), world
+    pre = il.run_tiled(store, queries[: 3 * ALIGN], il.Params(), cfg)
+    assert np.array_equal(pre, full[: 3 * ALIGN])
+    idx = np.arange(0, m, m // 512)
+    truth = oracle.truth(store, queries[idx])
+    assert np.max(np.abs(full[idx] - truth) / np.abs(truth)) <= 1e-5
+
+
+@pytest.mark.parametrize("kind,prec,p", [("soa", "single", 2.0), ("aos", "single", 3.5),
+                                         ("soa", "double", 2.0), ("hybrid", "double", 3.5),
+                                         ("aoas", "single", 1.0)])
+def test_fast_tiled_shards_all_arith(il, kind, prec, p):
+    """Every FAST tiled arithmetic (fp32 shared reciprocal, fp32 general and
+    integer p, fp64 p = 2 and quarter-root p) at a multi-chunk size."""
+    n, m = 300_000, 20_000
+    store, queries = cloud(il, n, m, kind, prec)
+    cfg = il.ExecConfig(mode="fast")
+    full = il.run_tiled(store, queries, il.Params(p), cfg)
+    got = sharded(il, il.run_tiled, store, queries, 8, il.Params(p), cfg)
+    assert np.array_equal(got, full)
+    # a query's value does not depend on the rest of the call
+    sub = il.run_tiled(store, queries[ALIGN : 5 * ALIGN], il.Params(p), cfg)
+    assert np.array_equal(sub, full[ALIGN : 5 * ALIGN])
+
+
+def test_fast_tiled_zero_eps_shards(il):
+    """zero_eps > 0: the per-chunk hit flag rides the fold (NaN partial) and
+    the fix-up returns the coincident z exactly, for any shard layout."""
+    n, m = 100_000, 8_192
+    store, queries = cloud(il, n, m)
+    x, y, z = store.component_views()
+    queries[::97] = np.column_stack([x[: len(queries[::97])], y[: len(queries[::97])]])
+    prm = il.Params(2.0, 1e-12)
+    cfg = il.ExecConfig(mode="fast")
+    full = il.run_tiled(store, queries, prm, cfg)
+    got = sharded(il, il.run_tiled, store, queries, 4, prm, cfg)
+    assert np.array_equal(got, full)
+    ref = oracle.predict(store, queries[::97], 2.0, 1e-12)
+    assert np.array_equal(full[::97], ref)
+
+
+@pytest.mark.parametrize("variant", ["run_naive", "run_nested_improved", "run_nested_original"])
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_other_variants_shards(il, variant, mode):
+    n, m = 200_000, 4_096
+    store, queries = cloud(il, n, m)
+    cfg = il.ExecConfig(mode=mode)
+    fn = getattr(il, variant)
+    full = fn(store, queries, il.Params(), cfg)
+    got = sharded(il, fn, store, queries, 8, il.Params(), cfg)
+    assert np.array_equal(got, full)
+
+
+def test_exact_tiled_shards(il):
+    n, m = 200_000, 10_000
+    store, queries = cloud(il, n, m, "soa", "single")
+    cfg = il.ExecConfig(mode="exact")
+    full = il.run_tiled(store, queries, il.Params(), cfg)
+    got = sharded(il, il.run_tiled, store, queries, 8, il.Params(), cfg)
+    assert np.array_equal(got, full)
+    assert np.array_equal(full[::1000], oracle.predict(store, queries[::1000]))
