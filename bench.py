@@ -426,67 +426,61 @@ def run_ours(args):
         except (KeyError, ValueError):
             pass
 
-    # ---- e2e through the public drop-in API (host buffers, blocking)
+    # ---- e2e through the public drop-in API (host buffers, blocking).  At
+    # N > 1 the drop-in's own multi-GPU form runs: rank 0 makes ONE run_*
+    # call over ExecConfig(devices=(0..N-1)) -- the store host->device once,
+    # the peer-copy broadcast tree, N query shards on N GPUs, each shard
+    # copied into its slice of the result -- while the other ranks wait at a
+    # barrier (their GPUs are the call's devices 1..N-1).
     e2e = e2e_pageable = None
     if not args.no_e2e:
         fn = il.STRATEGIES[variant]
-        local_store = store
-        if local_store is None:  # non-source ranks rebuild their host copy from HBM
-            raw = [t[:nb].cpu().numpy() for t, nb in zip(bufs, meta.nbytes)]
-            local_store = il.LayoutStore(il.LayoutKind(layout), il.Precision(prec), n, raw,
-                                         il.buffer_shapes(il.LayoutKind(layout), il.Precision(prec), n))
-        # pinned host copies of the store buffers (inputs of every step)
-        pinned = []
-        for b in local_store.buffers:
-            t = torch.empty(b.nbytes, dtype=torch.uint8, pin_memory=True)
-            t.numpy()[:] = b
-            pinned.append(t.numpy())
-        hstore = il.LayoutStore(local_store.kind, local_store.precision, n, pinned, local_store.shapes)
-        hq = np.ascontiguousarray(queries[lo:hi])
-        for _ in range(min(args.warmup, 2)):
-            fn(hstore, hq, params, cfg)
+        # (--device-override: every rank on one GPU, so the list repeats it)
+        e2e_devs = tuple(range(world)) if args.device_override is None else (args.device_override,) * world
+        cfg_e2e = il.ExecConfig(mode=args.mode, devices=e2e_devs) if world > 1 else cfg
+        if dist is not None:
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+        if rank == 0:
+            # pinned host copies of the store buffers (inputs of every step)
+            pinned = []
+            for b in store.buffers:
+                t = torch.empty(b.nbytes, dtype=torch.uint8, pin_memory=True)
+                t.numpy()[:] = b
+                pinned.append(t.numpy())
+            hstore = il.LayoutStore(store.kind, store.precision, n, pinned, store.shapes)
+            hq = np.ascontiguousarray(queries)
+            pstore = il.LayoutStore(store.kind, store.precision, n,
+                                    [np.array(b, copy=True) for b in store.buffers], store.shapes)
+
+            def timed(st_):
+                for _ in range(min(args.warmup, 2)):
+                    fn(st_, hq, params, cfg_e2e)
+                t0 = time.perf_counter()
+                for _ in range(args.steps):
+                    res = fn(st_, hq, params, cfg_e2e)
+                dt = time.perf_counter() - t0
+                del res
+                return dt
+
+            t_e2e = timed(hstore)
+            # the same through the caller's plain (pageable) numpy buffers: the
+            # reference's own run_* callers hold ordinary arrays
+            t_pg = timed(pstore)
+            e = 4 if prec == "single" else 8
+            # store buffers + the (m, 2) float64 query pairs (cast on the device, idw_run_xy)
+            h2d = sum(b.nbytes for b in hstore.buffers) + 16 * m
+            d2h = m * e
+            api = (f"paper_1402_4986_b200.{fn.__name__}(LayoutStore[pinned host], queries[host f64], "
+                   f"Params(p={p}), ExecConfig(mode='{args.mode}'"
+                   + (f", devices={e2e_devs}))" if world > 1 else "))"))
+            e2e = {"value": total_pairs * args.steps / t_e2e / 1e9, "unit": "GPairs/s",
+                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "api": api}
+            e2e_pageable = {"value": total_pairs * args.steps / t_pg / 1e9, "unit": "GPairs/s",
+                            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                            "api": api.replace("pinned host", "pageable host")}
         if dist is not None:
             dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            res = fn(hstore, hq, params, cfg)
-        t_e2e = time.perf_counter() - t0
-        if dist is not None:
-            t = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_e2e = float(t.item())
-        e = 4 if prec == "single" else 8
-        # store buffers + the (m, 2) float64 query pairs (cast on the device, idw_run_xy)
-        h2d = sum(b.nbytes for b in hstore.buffers) + 16 * (hi - lo)
-        d2h = (hi - lo) * e
-        h2d_all, d2h_all = h2d, d2h
-        if dist is not None:
-            t = torch.tensor([h2d, d2h], device=dev, dtype=torch.float64)
-            dist.all_reduce(t)
-            h2d_all, d2h_all = int(t[0].item()), int(t[1].item())
-        e2e = {"value": total_pairs * args.steps / t_e2e / 1e9, "unit": "GPairs/s",
-               "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": int(d2h_all),
-               "api": f"paper_1402_4986_b200.{fn.__name__}(LayoutStore[pinned host], queries[host f64], "
-                      f"Params(p={p}), ExecConfig(mode='{args.mode}'))"}
-        # the same through the caller's plain (pageable) numpy buffers: the
-        # reference's own run_* callers hold ordinary arrays
-        pstore = il.LayoutStore(local_store.kind, local_store.precision, n,
-                                [np.array(b, copy=True) for b in local_store.buffers], local_store.shapes)
-        fn(pstore, hq, params, cfg)
-        if dist is not None:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            res = fn(pstore, hq, params, cfg)
-        t_pg = time.perf_counter() - t0
-        if dist is not None:
-            t = torch.tensor([t_pg], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_pg = float(t.item())
-        e2e_pageable = {"value": total_pairs * args.steps / t_pg / 1e9, "unit": "GPairs/s",
-                        "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": int(d2h_all),
-                        "api": e2e["api"].replace("pinned host", "pageable host")}
-        del res
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None

@@ -38,7 +38,10 @@
 extern "C" {
 #endif
 
-#define IDW_ABI_VERSION 1
+#define IDW_ABI_VERSION 2
+
+/* Most query shards (device-list entries) one host-buffer call can drive. */
+#define IDW_MAX_DEVICES 16
 
 /* Layout kind codes == layouts._KIND_CODES (enum order, layouts.py:43-65). */
 enum idw_kind { IDW_SOA = 0, IDW_AOS = 1, IDW_AOAS = 2, IDW_SOAOS = 3, IDW_HYBRID = 4 };
@@ -95,8 +98,18 @@ typedef struct idw_params {
   int32_t mode;            /* enum idw_mode                                   */
   int64_t group_size;      /* G (nested lanes per query; tiled query group)   */
   int64_t tile_size;       /* T (reference staging tile; informational)       */
-  int32_t splits;          /* FAST tiled: data splits (0 = auto, 1 = none)    */
-  int32_t device;          /* CUDA device ordinal for this call               */
+  int32_t splits;          /* FAST tiled: summation chunks (0 = auto, from n) */
+  int32_t device;          /* CUDA device ordinal when ndevices == 0          */
+  /* Device list (host-buffer calls idw_run / idw_run_xy only; ABI 2).  Entry
+   * k evaluates query shard k: contiguous, whole 256-query units, sizes
+   * within one unit (partition.shard_bounds).  The store goes host->device
+   * once, to devices[0], and reaches the others by a cudaMemcpyPeerAsync
+   * broadcast tree; each entry runs on its own stream and copies its
+   * predictions straight into its slice of `out`.  Repeats are allowed (two
+   * streams on one GPU).  Results are bit-identical for every list: no
+   * query's arithmetic depends on its shard.  ndevices == 0 -> `device`.    */
+  int32_t ndevices;
+  int32_t devices[IDW_MAX_DEVICES];
 } idw_params;
 
 /* Optional per-call instrumentation (RunStats, strategies.py:104-115). */
@@ -118,9 +131,12 @@ const char *idw_last_error(void);
 
 /* Blocking run over HOST memory: copies the store buffers and the query
  * coordinates (qx, qy: m values of the run dtype each, already cast RN as in
- * strategies._prepare, strategies.py:125-134) to the device, runs the variant,
- * and writes m run-dtype predictions into `out`.  `stats` may be NULL.
- * Replaces one whole strategies.run_* call body.                          */
+ * strategies._prepare, strategies.py:125-134) to the device(s), runs the
+ * variant, and writes m run-dtype predictions into `out`.  `stats` may be
+ * NULL (kernel_ms: the slowest device's kernels).  One host thread drives
+ * every device of prm->devices (the reference's worker pool over query
+ * blocks, strategies.py:41-66,137-145).  Replaces one whole
+ * strategies.run_* call body.                                              */
 int idw_run(const idw_store *store, const void *qx, const void *qy, int64_t m,
             const idw_params *prm, void *out, idw_stats *stats);
 
@@ -136,7 +152,8 @@ int idw_run_xy(const idw_store *store, const double *queries, int64_t m,
                const idw_params *prm, void *out, idw_stats *stats);
 
 /* Asynchronous run over DEVICE memory on `stream` (a cudaStream_t, NULL =
- * legacy default stream).  Store buffers must stay readable up to
+ * legacy default stream), on one device (prm->device, or prm->devices[0]
+ * when prm->ndevices == 1; a longer list is IDW_E_ARG).  Store buffers must stay readable up to
  * nbytes rounded up to 16 bytes (bulk copies move 16-byte granules).  Scratch
  * is stream-ordered (cudaMallocAsync).  stats->kernel_ms is not filled here. */
 int idw_run_device(const idw_store *store, const void *qx, const void *qy, int64_t m,

@@ -15,7 +15,7 @@ from pathlib import Path
 
 import numpy as np
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # enum codes -- include/idw_b200.h
 KIND_CODES = {"soa": 0, "aos": 1, "aoas": 2, "soaos": 3, "hybrid": 4}  # layouts.py:65
@@ -48,6 +48,8 @@ class IdwParams(ctypes.Structure):
         ("tile_size", ctypes.c_int64),
         ("splits", ctypes.c_int32),
         ("device", ctypes.c_int32),
+        ("ndevices", ctypes.c_int32),
+        ("devices", ctypes.c_int32 * 16),
     ]
 
 
@@ -155,8 +157,12 @@ def make_store(kind: str, precision: str, count: int, pointers, nbytes) -> IdwSt
     return s
 
 
+MAX_DEVICES = 16  # IDW_MAX_DEVICES
+
+
 def make_params(p: float, zero_eps: float, variant: str, mode: str, group_size: int,
-                tile_size: int, splits: int = 0, device: int = 0) -> IdwParams:
+                tile_size: int, splits: int = 0, device: int = 0,
+                devices: tuple | None = None) -> IdwParams:
     prm = IdwParams()
     prm.p = float(p)
     prm.zero_eps = float(zero_eps)
@@ -166,6 +172,12 @@ def make_params(p: float, zero_eps: float, variant: str, mode: str, group_size: 
     prm.tile_size = int(tile_size)
     prm.splits = int(splits)
     prm.device = int(device)
+    devs = tuple(devices or ())
+    if len(devs) > MAX_DEVICES:
+        raise ValueError(f"at most {MAX_DEVICES} devices per call")
+    prm.ndevices = len(devs)
+    for i, d in enumerate(devs):
+        prm.devices[i] = int(d)
     return prm
 
 

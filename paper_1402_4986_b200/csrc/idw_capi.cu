@@ -6,6 +6,7 @@
 // per-device stream, and copy the predictions back.  No CPU fallback exists.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -91,8 +92,15 @@ static int validate(const idw_store *s, const void *qx, const void *qy, int64_t 
   if (p->group_size < 1) return set_error("group_size must be >= 1"), IDW_E_ARG;  // strategies.py:57-58
   if (p->tile_size < 1) return set_error("tile_size must be >= 1"), IDW_E_ARG;
   if (p->splits < 0) return set_error("splits must be >= 0"), IDW_E_ARG;
+  if (p->ndevices < 0 || p->ndevices > IDW_MAX_DEVICES)
+    return set_error("ndevices must be in [0, " + std::to_string(IDW_MAX_DEVICES) + "]"), IDW_E_ARG;
+  if (device_ptrs && p->ndevices > 1)
+    return set_error("a device list needs host buffers (idw_run / idw_run_xy)"), IDW_E_ARG;
   return 0;
 }
+
+// The one device of a device-pointer call.
+static int single_device(const idw_params *p) { return p->ndevices >= 1 ? p->devices[0] : p->device; }
 
 static std::mutex g_mu;
 
@@ -257,11 +265,12 @@ int idw_run_device(const idw_store *s, const void *qx, const void *qy, int64_t m
   if (m == 0) return 0;
   cudaStream_t dst;
   int sms;
-  if ((rc = device_stream(p->device, &dst, &sms))) return rc;
+  const int dev = single_device(p);
+  if ((rc = device_stream(dev, &dst, &sms))) return rc;
   Launch L;
   fill_launch(L, s, s->buf, qx, qy, m, p, out);
   L.st = (cudaStream_t)stream;
-  L.dev = p->device;
+  L.dev = dev;
   L.sms = sms;
   unsigned char *flags = nullptr;
   StreamFree free_flags;
@@ -271,103 +280,238 @@ int idw_run_device(const idw_store *s, const void *qx, const void *qy, int64_t m
     free_flags.p = flags;
     free_flags.st = L.st;
   }
-  EvSet &ev = g_ev[p->device];
+  EvSet &ev = g_ev[dev];
   if (!ev.a) {
     IDW_CK(cudaEventCreate(&ev.a));
     IDW_CK(cudaEventCreate(&ev.b));
     IDW_CK(cudaEventCreate(&ev.c));
   }
   rc = dispatch(L, &ev);
-  g_last_dev = rc == 0 ? p->device : -1;
+  g_last_dev = rc == 0 ? dev : -1;
   fill_stats(stats, L, p, s->count, m);
   return rc;
 }
 
+// Query shard k of `slots`: contiguous, whole 256-query units (a multiple of
+// every kernel's query group, so no group straddles two shards), sizes within
+// one unit -- partition.shard_bounds(m, slots, k, 256).
+static void shard_of(int64_t m, int slots, int k, int64_t *lo, int64_t *hi) {
+  const int64_t A = 256, units = (m + A - 1) / A, base = units / slots, extra = units % slots;
+  const int64_t lu = k * base + std::min<int64_t>(k, extra);
+  const int64_t hu = lu + base + (k < extra ? 1 : 0);
+  *lo = std::min<int64_t>(m, lu * A);
+  *hi = std::min<int64_t>(m, hu * A);
+}
+
+// Stream of the k-th use of `dev` in one call (k = 0: the device's stream).
+static int slot_stream(int dev, int k, cudaStream_t *st, int *sms) {
+  int rc = device_stream(dev, st, sms);
+  if (rc || k == 0) return rc;
+  static cudaStream_t extra[64][IDW_MAX_DEVICES];
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!extra[dev][k]) IDW_CK(cudaStreamCreateWithFlags(&extra[dev][k], cudaStreamNonBlocking));
+  *st = extra[dev][k];
+  return 0;
+}
+
+// Peer access between every pair of distinct listed devices (NVLink when the
+// pair has it; cudaMemcpyPeerAsync works either way).  Enabled once.
+static void enable_peers(const int32_t *devs, int n) {
+  static bool done[64][64];
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const int a = devs[i], b = devs[j];
+      if (a == b || done[a][b]) continue;
+      done[a][b] = true;
+      int ok = 0;
+      if (cudaDeviceCanAccessPeer(&ok, a, b) == cudaSuccess && ok && cudaSetDevice(a) == cudaSuccess)
+        cudaDeviceEnablePeerAccess(b, 0);  // AlreadyEnabled is fine
+      cudaGetLastError();
+    }
+}
+
+// One entry of a host call's device list: its stream, query shard and arena.
+struct Slot {
+  int dev = 0, sms = 0;
+  cudaStream_t st = nullptr;
+  int64_t lo = 0, hi = 0;
+  unsigned char *arena = nullptr;
+  size_t off[10] = {};
+  cudaEvent_t have_data = nullptr, e0 = nullptr, e1 = nullptr;
+  Launch L;
+  unsigned long long nfix = 0;
+  unsigned int bad = 0;
+};
+
 // Host-buffer path shared by idw_run (cast qx/qy given) and idw_run_xy (the
-// reference's (m, 2) float64 query array, split + cast + checked on device).
+// reference's (m, 2) float64 query array, split + cast + checked on device),
+// over one device or a device list driven from this one host thread:
+//   A. per entry: stream, query shard, one stream-ordered arena
+//   B. store: host -> devices[0], then a binomial broadcast tree of
+//      cudaMemcpyPeerAsync (round r: entries [0, 2^r) feed [2^r, 2^(r+1)))
+//   C. per entry: its query shard host -> device, kernels
+//   D. per entry: predictions device -> its slice of the caller's `out`
+// B-C are asynchronous across entries; D comes after every entry's C was
+// issued (a copy into pageable memory returns only when it is done).
 static int run_host(const idw_store *s, const void *qx, const void *qy, const double *xy, int64_t m,
                     const idw_params *p, void *out, idw_stats *stats) {
-  cudaStream_t st;
-  int sms, rc;
-  if ((rc = device_stream(p->device, &st, &sms))) return rc;
+  const int nslot = p->ndevices > 0 ? p->ndevices : 1;
+  const int32_t *devs = p->ndevices > 0 ? p->devices : &p->device;
   const size_t esz = s->precision == IDW_SINGLE ? 4 : 8;
-  // one stream-ordered arena: buffers (padded to 16 B + 64 B slack for the
-  // rounded-up bulk copy of the tail tile), qx, qy, out, flags, fix-up
-  // counter, non-finite flag, raw xy pairs
-  size_t off[10], total = 0;
-  auto take = [&](size_t bytes) {
-    size_t o = total;
-    total += (bytes + 255) & ~size_t(255);
-    return o;
-  };
-  for (int b = 0; b < s->nbuf; ++b) off[b] = take((size_t)s->nbytes[b] + 64);
-  off[3] = take(esz * (size_t)m);
-  off[4] = take(esz * (size_t)m);
-  off[5] = take(esz * (size_t)m);
-  off[6] = take((size_t)m);
-  off[7] = take(sizeof(unsigned long long));
-  off[8] = take(sizeof(unsigned int));
-  off[9] = xy ? take(2 * sizeof(double) * (size_t)m) : 0;
-  unsigned char *arena = nullptr;
-  IDW_CK(cudaMallocAsync((void **)&arena, total, st));
-  // the arena goes back to the pool on every exit, early error returns included
-  struct ArenaGuard {
-    unsigned char *p;
-    cudaStream_t st;
-    ~ArenaGuard() { cudaFreeAsync(p, st); }
-  } guard{arena, st};
-  const void *dbuf[3] = {nullptr, nullptr, nullptr};
-  for (int b = 0; b < s->nbuf; ++b) {
-    IDW_CK(cudaMemcpyAsync(arena + off[b], s->buf[b], (size_t)s->nbytes[b], cudaMemcpyHostToDevice, st));
-    dbuf[b] = arena + off[b];
-  }
-  unsigned int *bad = (unsigned int *)(arena + off[8]);
-  IDW_CK(cudaMemsetAsync(arena + off[7], 0, 256 + 256, st));  // nfixed + bad (adjacent 256-B slots)
-  if (xy) {
-    IDW_CK(cudaMemcpyAsync(arena + off[9], xy, 2 * sizeof(double) * (size_t)m, cudaMemcpyHostToDevice, st));
-    if ((rc = split_queries((const double *)(arena + off[9]), m, s->precision, arena + off[3], arena + off[4], bad,
-                            st, sms)))
-      return rc;
-  } else {
-    IDW_CK(cudaMemcpyAsync(arena + off[3], qx, esz * (size_t)m, cudaMemcpyHostToDevice, st));
-    IDW_CK(cudaMemcpyAsync(arena + off[4], qy, esz * (size_t)m, cudaMemcpyHostToDevice, st));
-  }
-  Launch L;
-  fill_launch(L, s, dbuf, arena + off[3], arena + off[4], m, p, arena + off[5]);
-  L.st = st;
-  L.dev = p->device;
-  L.sms = sms;
-  if (needs_fixup(L)) L.flags = arena + off[6];
-  L.nfixed = (unsigned long long *)(arena + off[7]);
-  // timing events: created once per device and host thread
-  static thread_local cudaEvent_t ev0[64] = {}, ev1[64] = {};
-  cudaEvent_t &e0 = ev0[p->device & 63], &e1 = ev1[p->device & 63];
-  if (!e0) IDW_CK(cudaEventCreate(&e0));
-  if (!e1) IDW_CK(cudaEventCreate(&e1));
-  IDW_CK(cudaEventRecord(e0, st));
-  rc = dispatch(L);
-  unsigned int nonfinite = 0;
-  if (rc == 0) {
-    IDW_CK(cudaEventRecord(e1, st));
-    IDW_CK(cudaMemcpyAsync(out, arena + off[5], esz * (size_t)m, cudaMemcpyDeviceToHost, st));
-    unsigned long long nfix = 0;
-    IDW_CK(cudaMemcpyAsync(&nfix, L.nfixed, sizeof(nfix), cudaMemcpyDeviceToHost, st));
-    IDW_CK(cudaMemcpyAsync(&nonfinite, bad, sizeof(nonfinite), cudaMemcpyDeviceToHost, st));
-    IDW_CK(cudaStreamSynchronize(st));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    if (stats) {
-      stats->kernel_ms = ms;
-      stats->fixup_queries = (int64_t)nfix;
+  Slot S[IDW_MAX_DEVICES];
+  int rc = 0;
+  // arenas and events go back on every exit, early error returns included
+  struct Guard {
+    Slot *S;
+    int n = 0;
+    bool sync = true;
+    ~Guard() {
+      for (int k = 0; k < n; ++k) {
+        cudaSetDevice(S[k].dev);
+        if (sync) cudaStreamSynchronize(S[k].st);
+        if (S[k].arena) cudaFreeAsync(S[k].arena, S[k].st);
+      }
+      cudaGetLastError();
     }
+  } guard{S};
+  int uses[64] = {};
+  for (int k = 0; k < nslot; ++k) {
+    if (devs[k] < 0 || devs[k] >= 64) return set_error("device ordinal out of range"), IDW_E_ARG;
+    Slot &sl = S[k];
+    sl.dev = devs[k];
+    if ((rc = slot_stream(sl.dev, uses[sl.dev]++, &sl.st, &sl.sms))) return rc;
+    shard_of(m, nslot, k, &sl.lo, &sl.hi);
   }
-  if (rc != 0) cudaStreamSynchronize(st);  // the guard frees the arena, stream-ordered
-  fill_stats(stats, L, p, s->count, m);
-  if (rc == 0 && nonfinite) {
+  if (nslot > 1) enable_peers(devs, nslot);
+  // per-(device, entry) events, created once per host thread
+  static thread_local cudaEvent_t evs[64][IDW_MAX_DEVICES][3];
+  for (int d = 0; d < 64; ++d) uses[d] = 0;
+  for (int k = 0; k < nslot; ++k) {
+    Slot &sl = S[k];
+    IDW_CK(cudaSetDevice(sl.dev));
+    cudaEvent_t *e = evs[sl.dev][uses[sl.dev]++];
+    for (int i = 0; i < 3; ++i)
+      if (!e[i]) IDW_CK(cudaEventCreate(&e[i]));
+    sl.have_data = e[0];
+    sl.e0 = e[1];
+    sl.e1 = e[2];
+  }
+
+  // A. arenas: buffers (+64 B slack for the rounded-up bulk copy of the tail
+  // tile), qx, qy, out, flags, fix-up counter, non-finite flag, raw xy pairs
+  for (int k = 0; k < nslot; ++k) {
+    Slot &sl = S[k];
+    const size_t mk = (size_t)(sl.hi - sl.lo);
+    size_t total = 0;
+    auto take = [&](size_t bytes) {
+      size_t o = total;
+      total += (bytes + 255) & ~size_t(255);
+      return o;
+    };
+    for (int b = 0; b < s->nbuf; ++b) sl.off[b] = take((size_t)s->nbytes[b] + 64);
+    sl.off[3] = take(esz * mk);
+    sl.off[4] = take(esz * mk);
+    sl.off[5] = take(esz * mk);
+    sl.off[6] = take(mk);
+    sl.off[7] = take(sizeof(unsigned long long));
+    sl.off[8] = take(sizeof(unsigned int));
+    sl.off[9] = xy ? take(2 * sizeof(double) * mk) : 0;
+    IDW_CK(cudaSetDevice(sl.dev));
+    IDW_CK(cudaMallocAsync((void **)&sl.arena, total, sl.st));
+    guard.n = k + 1;
+  }
+
+  // B. the store: one host->device copy, then the peer broadcast tree
+  IDW_CK(cudaSetDevice(S[0].dev));
+  for (int b = 0; b < s->nbuf; ++b)
+    IDW_CK(cudaMemcpyAsync(S[0].arena + S[0].off[b], s->buf[b], (size_t)s->nbytes[b], cudaMemcpyHostToDevice,
+                           S[0].st));
+  IDW_CK(cudaEventRecord(S[0].have_data, S[0].st));
+  for (int j = 1; j < nslot; ++j) {
+    int top = 1;
+    while (top * 2 <= j) top *= 2;
+    const Slot &src = S[j - top];
+    Slot &dst = S[j];
+    IDW_CK(cudaSetDevice(dst.dev));
+    IDW_CK(cudaStreamWaitEvent(dst.st, src.have_data, 0));
+    for (int b = 0; b < s->nbuf; ++b)
+      IDW_CK(cudaMemcpyPeerAsync(dst.arena + dst.off[b], dst.dev, src.arena + src.off[b], src.dev,
+                                 (size_t)s->nbytes[b], dst.st));
+    IDW_CK(cudaEventRecord(dst.have_data, dst.st));
+  }
+
+  // C. queries in, kernels
+  for (int k = 0; k < nslot; ++k) {
+    Slot &sl = S[k];
+    const int64_t mk = sl.hi - sl.lo;
+    if (mk == 0) continue;
+    IDW_CK(cudaSetDevice(sl.dev));
+    unsigned char *A = sl.arena;
+    IDW_CK(cudaMemsetAsync(A + sl.off[7], 0, 256 + 256, sl.st));  // nfixed + bad (adjacent 256-B slots)
+    if (xy) {
+      IDW_CK(cudaMemcpyAsync(A + sl.off[9], xy + 2 * sl.lo, 2 * sizeof(double) * (size_t)mk,
+                             cudaMemcpyHostToDevice, sl.st));
+      if ((rc = split_queries((const double *)(A + sl.off[9]), mk, s->precision, A + sl.off[3], A + sl.off[4],
+                              (unsigned int *)(A + sl.off[8]), sl.st, sl.sms)))
+        return rc;
+    } else {
+      IDW_CK(cudaMemcpyAsync(A + sl.off[3], (const char *)qx + esz * sl.lo, esz * (size_t)mk,
+                             cudaMemcpyHostToDevice, sl.st));
+      IDW_CK(cudaMemcpyAsync(A + sl.off[4], (const char *)qy + esz * sl.lo, esz * (size_t)mk,
+                             cudaMemcpyHostToDevice, sl.st));
+    }
+    const void *dbuf[3] = {nullptr, nullptr, nullptr};
+    for (int b = 0; b < s->nbuf; ++b) dbuf[b] = A + sl.off[b];
+    Launch &L = sl.L;
+    fill_launch(L, s, dbuf, A + sl.off[3], A + sl.off[4], mk, p, A + sl.off[5]);
+    L.st = sl.st;
+    L.dev = sl.dev;
+    L.sms = sl.sms;
+    if (needs_fixup(L)) L.flags = A + sl.off[6];
+    L.nfixed = (unsigned long long *)(A + sl.off[7]);
+    IDW_CK(cudaEventRecord(sl.e0, sl.st));
+    if ((rc = dispatch(L))) return rc;
+    IDW_CK(cudaEventRecord(sl.e1, sl.st));
+  }
+
+  // D. predictions out, straight into each entry's slice of `out`
+  for (int k = 0; k < nslot; ++k) {
+    Slot &sl = S[k];
+    const int64_t mk = sl.hi - sl.lo;
+    if (mk == 0) continue;
+    IDW_CK(cudaSetDevice(sl.dev));
+    IDW_CK(cudaMemcpyAsync((char *)out + esz * sl.lo, sl.arena + sl.off[5], esz * (size_t)mk,
+                           cudaMemcpyDeviceToHost, sl.st));
+    IDW_CK(cudaMemcpyAsync(&sl.nfix, sl.arena + sl.off[7], sizeof(sl.nfix), cudaMemcpyDeviceToHost, sl.st));
+    IDW_CK(cudaMemcpyAsync(&sl.bad, sl.arena + sl.off[8], sizeof(sl.bad), cudaMemcpyDeviceToHost, sl.st));
+  }
+  float kms = 0.f;
+  int64_t nfix = 0, launches = 0;
+  unsigned int nonfinite = 0;
+  for (int k = 0; k < nslot; ++k) {
+    Slot &sl = S[k];
+    IDW_CK(cudaSetDevice(sl.dev));
+    IDW_CK(cudaStreamSynchronize(sl.st));
+    if (sl.hi == sl.lo) continue;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, sl.e0, sl.e1) == cudaSuccess) kms = std::max(kms, ms);
+    nfix += (int64_t)sl.nfix;
+    nonfinite |= sl.bad;
+    launches += sl.L.launches;
+  }
+  guard.sync = false;
+  if (stats) {
+    stats->kernel_ms = kms;
+    stats->fixup_queries = nfix;
+    stats->kernel_launches = launches;
+    stats->merge_events = p->variant == IDW_NESTED_ORIGINAL ? m * ((s->count + p->group_size - 1) / p->group_size) : 0;
+  }
+  if (nonfinite) {
     set_error("invalid coordinate");  // core.ensure_finite (core.py:113-116)
     return IDW_E_NONFINITE;
   }
-  return rc;
+  return 0;
 }
 
 static void plan_free(idw_plan *pl) {
@@ -390,9 +534,10 @@ int idw_plan_create(const idw_store *s, const void *qx, const void *qy, int64_t 
   if (m == 0) return set_error("a plan needs at least one query"), IDW_E_ARG;
   cudaStream_t dst;
   int sms;
-  if ((rc = device_stream(p->device, &dst, &sms))) return rc;
+  const int dev = single_device(p);
+  if ((rc = device_stream(dev, &dst, &sms))) return rc;
   idw_plan *pl = new idw_plan();
-  pl->dev = p->device;
+  pl->dev = dev;
   cudaStream_t cap = nullptr;
   auto fail = [&](int code) {
     if (cap) {
@@ -414,7 +559,7 @@ int idw_plan_create(const idw_store *s, const void *qx, const void *qy, int64_t 
   Launch L;
   fill_launch(L, s, s->buf, qx, qy, m, p, out);
   L.st = cap;
-  L.dev = p->device;
+  L.dev = dev;
   L.sms = sms;
   unsigned char *flags = nullptr;
   if (needs_fixup(L)) {

@@ -8,7 +8,14 @@ all data (kernels.py:42-67), so the B200 design shards QUERIES:
   1. the data store is replicated by ONE broadcast of its raw layout buffers
      from the source rank (NCCL over NVLink/NVSwitch; gloo in CPU tests),
   2. each rank evaluates its contiguous query shard [lo, hi) on its own GPU,
-  3. the per-rank predictions are gathered to the root in rank order.
+  3. the per-rank predictions are gathered to the root in rank order (a
+     root gather: every rank sends only its own shard).
+
+This is the torchrun (one process per GPU) form of the job.  The drop-in
+call itself drives several GPUs from ONE process: ExecConfig(devices=...)
+-> idw_params.devices (include/idw_b200.h), with the store broadcast by a
+cudaMemcpyPeerAsync tree and each shard copied straight into the caller's
+output slice -- same shards (shard_bounds, align 256), same bits.
 
 There is no reduction, so every query keeps its single-device summation
 order and results are bit-identical for any world size, in both modes: EXACT
@@ -97,31 +104,32 @@ class QueryShardedRunner:
 
     # -- 3. gather --------------------------------------------------------
     def gather(self, local, m: int):
-        """all_gather of equal-size (padded) shards; the root trims and
-        concatenates in rank order.  Returns the full vector on every rank."""
+        """Root gather of the shards in rank order (each rank sends only its
+        own predictions: m values reach the root once, not world x m as an
+        all-gather would).  Returns the full vector on the root, None
+        elsewhere.  Shards are padded to equal length for the collective."""
         import torch
 
         L = padded_shard(m, self.world, self.align)
-        buf = torch.zeros(L, dtype=local.dtype, device=local.device)
+        # gloo gathers host tensors; NCCL gathers in place on the GPUs
+        on = local.device if self._backend() == "nccl" else torch.device("cpu")
+        buf = torch.zeros(L, dtype=local.dtype, device=on)
         buf[: local.numel()].copy_(local)
-        full = torch.empty(L * self.world, dtype=local.dtype, device=local.device)
-        self.dist.all_gather_into_tensor(full, buf) if hasattr(self.dist, "all_gather_into_tensor") and \
-            self._supports_agit() else self._all_gather_list(full, buf)
-        parts = []
+        parts = [torch.empty_like(buf) for _ in range(self.world)] if self.rank == self.src else None
+        self.dist.gather(buf, gather_list=parts, dst=self.src)
+        if self.rank != self.src:
+            return None
+        out = []
         for r in range(self.world):
             lo, hi = shard_bounds(m, self.world, r, self.align)
-            parts.append(full[r * L: r * L + (hi - lo)])
-        return torch.cat(parts)
+            out.append(parts[r][: hi - lo])
+        return torch.cat(out)
 
-    def _supports_agit(self) -> bool:
+    def _backend(self) -> str:
         try:
-            return self.dist.get_backend() == "nccl"
+            return str(self.dist.get_backend())
         except Exception:  # pragma: no cover
-            return False
-
-    def _all_gather_list(self, full, buf):
-        chunks = list(full.chunk(self.world))
-        self.dist.all_gather(chunks, buf)
+            return "gloo"
 
     # -- whole job ----------------------------------------------------------
     def run(self, compute: Callable, buffers, meta: StoreMeta, qx_local, qy_local, m: int):

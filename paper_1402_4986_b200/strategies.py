@@ -9,13 +9,21 @@ underneath is one blocking call into libidw_b200 per strategy call:
     run_nested_improved  K3  G strided lanes + shuffle tree   (kernels.py:111-185)
     run_nested_original  K4  per-group tree + serial merge    (kernels.py:188-248)
 
-``ExecConfig`` gains three GPU knobs with reference-neutral defaults:
+``ExecConfig`` gains four GPU knobs with reference-neutral defaults:
 
     mode    "exact" (default; env IDW_MODE) -- IEEE RN ops in the reference's
             order: p = 2 results are bit-identical to the reference;
             "fast"  -- MUFU/FMA/f32x2 arithmetic, blocked compensated sums,
             exact fix-up of coincident queries; held to the tolerance table.
     device  CUDA ordinal (default env IDW_DEVICE or 0)
+    devices device list (default env IDW_DEVICES="0,1,..." or none): one host
+            thread drives them all from the one call -- the store goes to
+            devices[0] once and on by a peer-copy broadcast tree, entry k
+            evaluates the k-th 256-aligned query shard on its own stream and
+            writes its slice of the result.  This is the reference's worker
+            pool (``parallel_width`` threads over static query blocks,
+            strategies.py:41-66,137-145) with GPUs as the workers; results
+            are bit-identical for every list (repeats allowed).
     splits  FAST tiled summation chunks (0 = auto: a function of n alone).
             A nonzero value fixes the chunk count instead; it is part of the
             summation order, so it changes the FAST bits (still within the
@@ -53,6 +61,7 @@ class ExecConfig:
     mode: str | None = None
     device: int | None = None
     splits: int = 0
+    devices: tuple | None = None
 
     def __post_init__(self) -> None:
         if self.group_size < 1:
@@ -73,6 +82,14 @@ class ExecConfig:
             object.__setattr__(self, "device", int(os.environ.get("IDW_DEVICE", "0")))
         if self.splits < 0:
             raise ValueError("splits must be >= 0")
+        if self.devices is None and os.environ.get("IDW_DEVICES"):
+            object.__setattr__(self, "devices",
+                               tuple(int(d) for d in os.environ["IDW_DEVICES"].split(",") if d.strip()))
+        if self.devices is not None:
+            devs = tuple(int(d) for d in self.devices)
+            if not devs or len(devs) > _capi.MAX_DEVICES or min(devs) < 0:
+                raise ValueError(f"devices must list 1..{_capi.MAX_DEVICES} device ordinals >= 0")
+            object.__setattr__(self, "devices", devs)
 
 
 @dataclass
@@ -168,7 +185,7 @@ def _dispatch(variant: str, store, queries, params: Params, cfg: ExecConfig):
     qs = np.ascontiguousarray(qs)
     out = np.empty(qs.shape[0], dtype=dt)
     prm = _capi.make_params(params.p, params.zero_eps, variant, cfg.mode, cfg.group_size,
-                            cfg.tile_size, cfg.splits, cfg.device)
+                            cfg.tile_size, cfg.splits, cfg.device, cfg.devices)
     try:
         stats = _capi.run_host_xy(_native_store(store), qs, prm, out)
     except _capi.NativeError:

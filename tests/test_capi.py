@@ -33,13 +33,62 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
 
 
-def test_abi_version_and_struct_sizes():
+def test_abi_version_and_struct_layouts(tmp_path):
+    """ctypes mirrors of the header structs match the C compiler's layout
+    field by field (gcc on include/idw_b200.h)."""
     lib = _capi.load()
-    assert lib.idw_abi_version() == _capi.ABI_VERSION == 1
-    # struct layouts of the header (x86-64): idw_store 72, idw_params 48, idw_stats 32
-    assert ctypes.sizeof(_capi.IdwStore) == 72
-    assert ctypes.sizeof(_capi.IdwParams) == 48
-    assert ctypes.sizeof(_capi.IdwStats) == 32
+    assert lib.idw_abi_version() == _capi.ABI_VERSION == 2
+    structs = {"idw_store": _capi.IdwStore, "idw_params": _capi.IdwParams, "idw_stats": _capi.IdwStats}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append('printf("IDW_MAX_DEVICES %d\\n", IDW_MAX_DEVICES); return 0; }')
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    import subprocess
+    subprocess.run(["gcc", "-std=c11", "-o", str(exe), str(src)], check=True)
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                         check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[f"{cname} size"]) == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert int(got[f"{cname}.{f}"]) == getattr(py, f).offset, (cname, f)
+    assert int(got["IDW_MAX_DEVICES"]) == _capi.MAX_DEVICES == len(_capi.IdwParams().devices)
+
+
+def test_device_list_validation():
+    from paper_1402_4986_b200 import ExecConfig
+
+    assert ExecConfig(devices=[0, 0, 1]).devices == (0, 0, 1)
+    for bad in ((), (-1,), tuple(range(17))):
+        with pytest.raises(ValueError):
+            ExecConfig(devices=bad)
+    prm = _capi.make_params(2.0, 0.0, "tiled", "fast", 1024, 1024, 0, 0, (3, 1))
+    assert prm.ndevices == 2 and list(prm.devices[:2]) == [3, 1]
+    lib = _capi.load()
+    st = _store()
+    ns = _capi.make_store("soa", "double", st.count, [b.ctypes.data for b in st.buffers],
+                          [b.nbytes for b in st.buffers])
+    q = np.zeros(4)
+    # a device list is a host-buffer feature: device-pointer calls refuse it
+    rc = lib.idw_run_device(ctypes.byref(ns), q.ctypes.data, q.ctypes.data, 4, ctypes.byref(prm),
+                            q.ctypes.data, None, None)
+    assert rc == -1 and b"host buffers" in lib.idw_last_error()
+    prm.ndevices = 17
+    rc = lib.idw_run(ctypes.byref(ns), q.ctypes.data, q.ctypes.data, 4, ctypes.byref(prm), q.ctypes.data, None)
+    assert rc == -1 and b"ndevices" in lib.idw_last_error()
+
+
+def test_device_list_env(monkeypatch):
+    from paper_1402_4986_b200 import ExecConfig
+
+    monkeypatch.setenv("IDW_DEVICES", "0,2, 1")
+    assert ExecConfig().devices == (0, 2, 1)
+    monkeypatch.delenv("IDW_DEVICES")
+    assert ExecConfig().devices is None
 
 
 def _store(kind=LayoutKind.SoA, precision=Precision.double):

@@ -120,3 +120,59 @@ def test_exact_tiled_shards(il):
     got = sharded(il, il.run_tiled, store, queries, 8, il.Params(), cfg)
     assert np.array_equal(got, full)
     assert np.array_equal(full[::1000], oracle.predict(store, queries[::1000]))
+
+
+# ---- one call, a device list (ExecConfig.devices; idw_params.devices, ABI 2).
+# The 1-GPU box lists device 0 several times: every entry still gets its own
+# stream, arena, broadcast copy (a same-device cudaMemcpyPeerAsync) and query
+# shard, so the sharding, the broadcast tree and the gather into `out` run
+# exactly as on 8 GPUs.
+
+@pytest.mark.parametrize("variant,mode,kind,prec", [
+    ("run_tiled", "fast", "aoas", "single"), ("run_tiled", "exact", "soa", "single"),
+    ("run_naive", "fast", "aos", "double"), ("run_nested_improved", "fast", "soa", "single"),
+    ("run_nested_original", "exact", "hybrid", "double")])
+def test_device_list_bitwise(il, variant, mode, kind, prec):
+    n, m = 150_000, 5_000
+    store, queries = cloud(il, n, m, kind, prec)
+    fn = getattr(il, variant)
+    one = fn(store, queries, il.Params(), il.ExecConfig(mode=mode, devices=(0,)))
+    assert np.array_equal(one, fn(store, queries, il.Params(), il.ExecConfig(mode=mode)))
+    for devs in ((0, 0), (0, 0, 0), (0,) * 8):
+        stats = il.RunStats()
+        got = fn(store, queries, il.Params(), il.ExecConfig(mode=mode, devices=devs), stats)
+        assert np.array_equal(got, one), devs
+        if variant == "run_nested_original":
+            assert stats.merge_events == m * -(-n // 1024)
+
+
+def test_device_list_c3_fast(il):
+    """C3 through one run_tiled call over an 8-entry device list == one device."""
+    n = m = 1 << 20
+    store, queries = cloud(il, n, m)
+    one = il.run_tiled(store, queries, il.Params(), il.ExecConfig(mode="fast"))
+    got = il.run_tiled(store, queries, il.Params(), il.ExecConfig(mode="fast", devices=(0,) * 8))
+    assert np.array_equal(got, one)
+
+
+def test_device_list_edges(il):
+    """More entries than 256-query units (empty shards), the cast-query entry
+    point (idw_run), and the reference's ValueError for a non-finite query."""
+    store, queries = cloud(il, 50_000, 300)
+    cfg1 = il.ExecConfig(mode="fast")
+    one = il.run_tiled(store, queries, il.Params(), cfg1)
+    got = il.run_tiled(store, queries, il.Params(), il.ExecConfig(mode="fast", devices=(0,) * 5))
+    assert np.array_equal(got, one)
+    from paper_1402_4986_b200 import _capi
+    from paper_1402_4986_b200.strategies import _native_store
+
+    qx = queries[:, 0].astype(np.float32)
+    qy = queries[:, 1].astype(np.float32)
+    out = np.empty(len(qx), np.float32)
+    prm = _capi.make_params(2.0, 0.0, "tiled", "fast", 1024, 1024, 0, 0, (0, 0, 0))
+    _capi.run_host(_native_store(store), qx, qy, prm, out)
+    assert np.array_equal(out, one)
+    bad = queries.copy()
+    bad[299, 1] = np.inf
+    with pytest.raises(ValueError, match="invalid coordinate"):
+        il.run_tiled(store, bad, il.Params(), il.ExecConfig(mode="fast", devices=(0, 0)))
