@@ -508,3 +508,38 @@ def test_exact_split_reduce_subnormal_d2_bitwise_fp64(il):
             assert np.all(np.isfinite(ref[:6]))
             got = il.run_nested_improved(store, queries, cfg=il.ExecConfig(mode="exact", group_size=G))
             assert np.array_equal(got.view(np.uint8), ref.view(np.uint8)), (kind, G)
+
+
+def test_exact_fixup_many_subnormal_queries_1m(il):
+    """The strict-order recompute of flagged no-hit queries (EXACT naive and
+    tiled; reference predict_block, kernels.py:49-63) is batched: 32 queries
+    per block advance together through one pass over the data, their exact
+    weights computed block-wide and summed left to right by one lane each.
+    2048 queries a subnormal distance from a data point at n = 1M must come
+    back bitwise equal to the reference's sums, in well under a second."""
+    import time
+
+    n = 1 << 20
+    rng = np.random.default_rng(123)
+    data = random_records(rng, n, 0.0, 1.0)
+    data[:, :2] = 0.1 + 0.9 * data[:, :2]
+    data[12345] = (0.0, 0.0, 0.37)
+    k = 2048
+    deltas = 2.0 ** -rng.uniform(63.05, 63.99, k)
+    sub = np.where(rng.random(k)[:, None] < 0.5, np.column_stack([deltas, 0 * deltas]),
+                   np.column_stack([0 * deltas, deltas]))
+    queries = np.vstack([sub, random_queries(rng, 2048)])
+    store = il.build(data, il.LayoutKind.AoaS, il.Precision.single)
+    ref = oracle.predict_mt(store, queries)
+    assert np.all(np.isfinite(ref[:k]))
+    for s in ("tiled", "naive"):
+        fn = il.STRATEGIES[s]
+        cfg = il.ExecConfig(mode="exact")
+        fn(store, queries[:300], cfg=cfg)  # warm-up (pool pages, first launch)
+        st = il.RunStats()
+        t0 = time.perf_counter()
+        got = fn(store, queries, il.Params(), cfg, st)
+        dt = time.perf_counter() - t0
+        assert np.array_equal(got.view(np.uint8), ref.view(np.uint8)), s
+        assert st.fixup_queries >= k, (s, st.fixup_queries)
+        assert dt < 1.0, (s, dt)
