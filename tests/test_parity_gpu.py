@@ -54,6 +54,29 @@ def test_exact_mode_matches_reference_golden(il, golden, strategy):
                 assert rel(got, ref) <= TOL[precision.value], (name, kind, precision, strategy)
 
 
+def test_runstats_match_reference(il, golden):
+    """GPU-path RunStats (reference strategies.py:104-115, 202-261):
+    nested_original's merge_events equal the reference's own count for every
+    golden case (m * ceil(n/G), test_strategies.py:124-130), nested_improved
+    reports zero merges and G workers of ceil(n/G) trips each
+    (test_strategies.py:132-140, test_acceptance.py:97-109), in both modes."""
+    for name in _names(golden):
+        data, queries, p, eps, G, T = golden_case(golden, name)
+        for mode in ("exact", "fast"):
+            cfg = il.ExecConfig(group_size=G, tile_size=T, mode=mode)
+            for kind, precision in il.legal_pairs():
+                store = il.build(data, kind, precision)
+                rs = il.RunStats()
+                il.run_nested_original(store, queries, il.Params(p, eps), cfg, rs)
+                assert rs.merge_events == golden[f"{name}/{precision.value}/{kind.value}/merges"][0], (name, mode)
+                assert rs.kernel_launches >= 1
+                rs = il.RunStats()
+                il.run_nested_improved(store, queries, il.Params(p, eps), cfg, rs)
+                assert rs.merge_events == 0
+                assert rs.worker_trips is not None and len(rs.worker_trips) == G
+                assert np.all(rs.worker_trips == -(-len(data) // G)), (name, mode)
+
+
 def test_read_counters_match_reference(il, golden):
     for name in _names(golden):
         data, queries, p, eps, G, T = golden_case(golden, name)

@@ -5,7 +5,8 @@ each warp-trip reads 32 consecutive points with plain LDGs, the model's access
 pattern) on n = 32768 points x m = 1024 queries; under
 `ncu --metrics lts__t_sectors_srcunit_tex_op_read.sum,...` that gives measured
 sectors.  `python tools/xcheck_txn.py report <dir>` joins the ncu CSVs with
-count_transactions(segment_bytes=32) x warp-trips.
+the reference model's count_transactions(segment_bytes=32) x warp-trips
+(pinned in tests/golden/transactions_ref.json).
 """
 import csv, json, sys
 from pathlib import Path
@@ -27,14 +28,16 @@ if sys.argv[1] == "run":
         predict_device(ds, tq[0], tq[1], out, il.Params(), il.ExecConfig(mode="fast", group_size=G), "nested_improved")
     torch.cuda.synchronize()
 else:
-    from paper_1402_4986_b200.core import Precision
-    from paper_1402_4986_b200.layouts import LayoutKind
-    from paper_1402_4986_b200.transactions import AccessPattern, count_transactions
+    # the reference model's answers, pinned from the reference itself
+    # (tests/golden/make_txn_golden.py): the product carries no copy of it
+    fx = json.loads((ROOT / "tests" / "golden" / "transactions_ref.json").read_text())["cases"]
+    model = {c["layout"]: c for c in fx if (c["precision"], c["components"], c["warp"], c["segment"], c["base"])
+             == ("double", "xyz", 32, 32, 0)}
     d = Path(sys.argv[2])
     trips = (N // 32) * (M // Q)
     rows = []
     for L in LAYOUTS:
-        rep = count_transactions(AccessPattern(LayoutKind(L), Precision.double, ("x", "y", "z"), 32, 32))
+        rep = model[L]
         meas = {}
         f = d / f"xcheck_{L}.csv"
         if f.exists():
@@ -44,7 +47,7 @@ else:
         l2 = meas.get("lts__t_sectors_srcunit_tex_op_read.sum")
         l1 = meas.get("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum")
         ins = meas.get("smsp__inst_executed_op_global_ld.sum")
-        rows.append({"layout": L, "model_segments_per_warp_trip": rep.segments, "model_utilization": rep.utilization,
+        rows.append({"layout": L, "model_segments_per_warp_trip": rep["segments"], "model_utilization": rep["utilization"],
                      "measured_l2_to_l1_sectors_per_trip": None if l2 is None else l2 / trips,
                      "measured_l1_sectors_per_trip": None if l1 is None else l1 / trips,
                      "ld_instr_per_trip": None if ins is None else ins / trips})
