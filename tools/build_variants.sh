@@ -4,7 +4,7 @@
 set -e
 cd "$(dirname "$0")/../paper_1402_4986_b200/csrc"
 NVFLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr"
-OUT=../../build/variants
+OUT=../../build/nv
 mkdir -p $OUT
 # v = name:extra nvcc defines (comma separated), e.g. r0u8:-DIDW_NEST_RING32=0,-DIDW_NEST_U32=8
 for v in "$@"; do
