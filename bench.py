@@ -49,7 +49,7 @@ CONFIGS = {
     "c4": (1024 * K, 1024 * K, "soa", "double", "nested_improved", 3.5,
            "C4: 1M x 1M, p=3.5, fp64, SoA, split-reduce (K3)"),
     "c5": (10240 * K, 100 * K, "aoas", "single", "tiled", 2.0,
-           "C5: 10M data x 100K queries, p=2, fp32, AoaS, tiled (K2, data splits)"),
+           "C5: 10M data x 100K queries, p=2, fp32, AoaS, tiled (K2, chunked data)"),
 }
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 SHARD_ALIGN = 256

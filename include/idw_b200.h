@@ -190,7 +190,7 @@ int idw_pack_device(const double *x, const double *y, const double *z, int64_t n
 int idw_convert_device(const idw_store *src, const idw_store *dst, int device, void *stream);
 
 /* Device time of the last successful idw_run_device call on this thread:
- * the variant kernels (e.g. k_tiled [+ k_combine]) and the FAST fix-up pass,
+ * the variant kernels (e.g. k_bbox + k_tiled_chunks) and the FAST fix-up pass,
  * from events recorded on the call's stream.  Blocks until they complete.   */
 int idw_last_kernel_ms(double *variant_ms, double *fixup_ms);
 
