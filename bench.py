@@ -438,9 +438,14 @@ def run_ours(args):
         # (--device-override: every rank on one GPU, so the list repeats it)
         e2e_devs = tuple(range(world)) if args.device_override is None else (args.device_override,) * world
         cfg_e2e = il.ExecConfig(mode=args.mode, devices=e2e_devs) if world > 1 else cfg
+        host_group = None
         if dist is not None:
             torch.cuda.synchronize(dev)
-            dist.barrier()
+            # the other ranks wait on a host-side (gloo) barrier: an NCCL
+            # barrier would leave a spinning collective kernel on the very
+            # GPUs rank 0's call is using
+            host_group = dist.new_group(backend="gloo")
+            dist.barrier(group=host_group)
         if rank == 0:
             # pinned host copies of the store buffers (inputs of every step)
             pinned = []
@@ -480,7 +485,7 @@ def run_ours(args):
                             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                             "api": api.replace("pinned host", "pageable host")}
         if dist is not None:
-            dist.barrier()
+            dist.barrier(group=host_group)
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
