@@ -1,7 +1,9 @@
 """Small runs of every variant / mode / precision for compute-sanitizer
 (memcheck, racecheck, synccheck): the smem rings of K2, the cp.async ring,
 cluster/DSMEM tree and persistent loop of K3, K4's trees, the fix-up and
-combine passes, the device packers/converters and a graph plan."""
+fix-up passes, the device packers/converters and a graph plan; round 2: the
+chunked K2 FAST scheduler (ring-slot reuse), K3's warp split, the
+device-list host path and the batched exact fix-up."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -25,4 +27,16 @@ for precision in il.Precision:
         out = torch.empty(len(queries), dtype=ds.dtype, device="cuda")
         plan = DevicePlan(ds, q[0], q[1], out, il.Params(), il.ExecConfig(mode="fast"), "tiled")
         plan.launch(); torch.cuda.synchronize(); plan.close()
+# round 2: K2 FAST chunk ring with slot reuse (groups > ring slots), the
+# device-list host path, the batched exact fix-up (subnormal d2, EXACT naive/tiled)
+x, y, z = il.generate_cloud_arrays(60_000, 0)
+qx, qy, _ = il.generate_cloud_arrays(60_000, 1)
+big = il.LayoutStore.from_arrays(x, y, z, il.LayoutKind.AoaS, il.Precision.single)
+il.run_tiled(big, np.column_stack([qx, qy]), cfg=il.ExecConfig(mode="fast"))
+il.run_tiled(big, np.column_stack([qx, qy])[:5000], cfg=il.ExecConfig(mode="fast", devices=(0, 0, 0)))
+sub = data.copy(); sub[:, :2] = 0.1 + 0.9 * sub[:, :2]; sub[7] = (0.0, 0.0, 0.37)
+qs = np.vstack([[[2.0 ** -63.5, 0.0], [0.0, 2.0 ** -63.2]], queries[:100]])
+st = il.build(sub, il.LayoutKind.SoA, il.Precision.single)
+for variant in ("naive", "tiled", "nested_improved"):
+    il.STRATEGIES[variant](st, qs, cfg=il.ExecConfig(mode="exact"))
 print("sanitize target done")
