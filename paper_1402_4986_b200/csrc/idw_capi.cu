@@ -361,6 +361,20 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
   const size_t esz = s->precision == IDW_SINGLE ? 4 : 8;
   Slot S[IDW_MAX_DEVICES];
   int rc = 0;
+  // the caller's current device is restored on every exit (a device list
+  // switches devices; the caller's framework may rely on its own setting)
+  struct DeviceRestore {
+    int dev = -1;
+    DeviceRestore() {
+      if (cudaGetDevice(&dev) != cudaSuccess) {
+        dev = -1;
+        cudaGetLastError();
+      }
+    }
+    ~DeviceRestore() {
+      if (dev >= 0) cudaSetDevice(dev);
+    }
+  } restore_device;
   // arenas and events go back on every exit, early error returns included
   struct Guard {
     Slot *S;
