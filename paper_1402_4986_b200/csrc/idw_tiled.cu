@@ -86,8 +86,8 @@ static void chunk_shape(long long ntiles, int forced, long long *S, long long *t
   *S = cdiv(ntiles, t);
 }
 
-template <int K, typename T, bool P2, bool EPS>
-static int launch_tiled_fast(Launch &L) {
+template <int K, typename T, bool P2, bool EPS, bool INLINE_BOX>
+static int launch_tiled_fast_box(Launch &L) {
   using C = TiledCfg<T, FAST>;
   constexpr int Q = C::Q, TILE = C::TILE, QG = 32 * Q, NC = 256;
   constexpr int RING = tiled_ring_bytes<K, T, TILE>();
@@ -99,8 +99,8 @@ static int launch_tiled_fast(Launch &L) {
     // MUFU and FMA-pipe work is best balanced at 1).  IDW_PROD overrides
     // (it changes which queries pair up, hence the bits).
     static const int prod = [] { const char *e = getenv("IDW_PROD"); return e ? atoi(e) : 1; }();
-    if (prod == 1) kern = k_tiled_chunks<K, T, P2, EPS, Q, TILE, 1>;
-    if (prod == 2) kern = k_tiled_chunks<K, T, P2, EPS, Q, TILE, 2>;
+    if (prod == 1) kern = k_tiled_chunks<K, T, P2, EPS, Q, TILE, 1, 0, INLINE_BOX>;
+    if (prod == 2) kern = k_tiled_chunks<K, T, P2, EPS, Q, TILE, 2, 0, INLINE_BOX>;
     prod_used = prod == 1 || prod == 2;
   }
   if constexpr (sizeof(T) == 8 && !P2) {
@@ -148,35 +148,50 @@ static int launch_tiled_fast(Launch &L) {
   // group is long folded when the slot comes round again
   const long long R = S > 1 ? std::min<long long>(groups, 4 * cdiv(warps, S) + 4) : 0;
 
-  // scratch: [next u64 | bbox counter u32 | pad | done[R] | gen[R] | partials]
+  // scratch: [next u64 | pad | done[R] | gen[R] | chunk boxes[S] | partials]
   const size_t ctl = ((size_t)(16 + 8 * R) + 255) / 256 * 256;
+  const size_t boxb = prod_used && !INLINE_BOX ? ((size_t)S * sizeof(float4) + 255) / 256 * 256 : 0;
   const size_t part = (size_t)R * (size_t)S * 2 * QG * sizeof(T);
   unsigned char *ws = nullptr;
-  StreamFree free_box, free_ws;  // scratch goes back to the pool on every exit
-  IDW_CK(cudaMallocAsync((void **)&ws, ctl + part, L.st));
+  StreamFree free_ws;  // scratch goes back to the pool on every exit
+  IDW_CK(cudaMallocAsync((void **)&ws, ctl + boxb + part, L.st));
   free_ws.p = ws;
   free_ws.st = L.st;
   IDW_CK(cudaMemsetAsync(ws, 0, ctl, L.st));
-  float4 *dbox = nullptr;
-  if (prod_used) {  // data box for the shared-reciprocal guard
-    if (int rc = launch_bbox<K, T>(L, &dbox, (unsigned int *)(ws + 8))) return rc;
-    free_box.p = dbox;
-    free_box.st = L.st;
+  float4 *boxes = boxb ? (float4 *)(ws + ctl) : nullptr;
+  if (boxes) {  // chunk data boxes for the shared-reciprocal guard
+    k_chunk_boxes<K, T><<<(unsigned)cdiv(S * 32, 256), 256, 0, L.st>>>(L.g, L.n, tpc * TILE, (int)S, boxes);
+    IDW_CK_LAUNCH();
+    ++L.launches;
   }
   ChunkSched<T> cs;
   cs.next = (unsigned long long *)ws;
   cs.done = (unsigned int *)(ws + 16);
   cs.gen = cs.done + R;
-  cs.part = (T *)(ws + ctl);
+  cs.boxes = boxes;
+  cs.part = (T *)(ws + ctl + boxb);
   cs.groups = groups;
   cs.S = (int)S;
   cs.tpc = (int)tpc;
   cs.R = (int)R;
   kern<<<(unsigned)blocks, threads, smem_l, L.st>>>(L.g, L.n, (const T *)L.qx, (const T *)L.qy, L.m,
-                                                    make_scal<T>(L), (T *)L.out, L.flags, cs, dbox);
+                                                    make_scal<T>(L), (T *)L.out, L.flags, cs);
   IDW_CK_LAUNCH();
   ++L.launches;
   return 0;
+}
+
+template <int K, typename T, bool P2, bool EPS>
+static int launch_tiled_fast(Launch &L) {
+  if constexpr (std::is_same<T, float>::value && P2 && !EPS) {
+    // a job whose (group, chunk) items fit one round of a full grid: each
+    // warp boxes its own chunk instead of waiting for a box pre-pass launch
+    using C = TiledCfg<T, FAST>;
+    long long S = 1, tpc = 1;
+    chunk_shape(cdiv(L.n, C::TILE), L.splits, &S, &tpc);
+    if (cdiv(L.m, 32 * C::Q) * S < (long long)L.sms * 16) return launch_tiled_fast_box<K, T, P2, EPS, true>(L);
+  }
+  return launch_tiled_fast_box<K, T, P2, EPS, false>(L);
 }
 
 template <int K, typename T, int MODE, bool P2, bool EPS, int Q>
