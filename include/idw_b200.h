@@ -100,7 +100,7 @@ typedef struct idw_params {
   int64_t tile_size;       /* T (reference staging tile; informational)       */
   int32_t splits;          /* FAST tiled: summation chunks (0 = auto, from n) */
   int32_t device;          /* CUDA device ordinal when ndevices == 0          */
-  /* Device list (host-buffer calls idw_run / idw_run_xy only; ABI 2).  Entry
+  /* Device list (ABI 2; idw_run / idw_run_xy / idw_run_device).  Entry
    * k evaluates query shard k: contiguous, whole 256-query units, sizes
    * within one unit (partition.shard_bounds).  The store goes host->device
    * once, to devices[0], and reaches the others by a cudaMemcpyPeerAsync
@@ -152,14 +152,18 @@ int idw_run_xy(const idw_store *store, const double *queries, int64_t m,
                const idw_params *prm, void *out, idw_stats *stats);
 
 /* Asynchronous run over DEVICE memory on `stream` (a cudaStream_t, NULL =
- * legacy default stream), on one device (prm->device, or prm->devices[0]
- * when prm->ndevices == 1; a longer list is IDW_E_ARG).  Store buffers must stay readable up to
+ * legacy default stream), on prm->device (or prm->devices[0]).  With
+ * prm->ndevices > 1 every pointer lives on devices[0] and the call spreads
+ * itself over the list: the store reaches the other entries by a
+ * cudaMemcpyPeerAsync broadcast tree, entry k's query shard by a peer copy,
+ * and its predictions come back into its slice of `out` by a peer copy (the
+ * gather); `stream` waits for all entries.  Store buffers must stay readable up to
  * nbytes rounded up to 16 bytes (bulk copies move 16-byte granules).  Scratch
  * is stream-ordered (cudaMallocAsync).  stats->kernel_ms is not filled here. */
 int idw_run_device(const idw_store *store, const void *qx, const void *qy, int64_t m,
                    const idw_params *prm, void *out, void *stream, idw_stats *stats);
 
-/* Plans: one idw_run_device call captured into a CUDA graph (the bounding-box
+/* Plans (one device: ndevices <= 1): one idw_run_device call captured into a CUDA graph (the bounding-box
  * pre-pass, the variant kernels, the fix-up pass and their stream-ordered
  * scratch), replayed by idw_plan_launch for ~3 us of host time instead of
  * one runtime call per kernel.  The plan keeps the store, query and output

@@ -94,8 +94,6 @@ static int validate(const idw_store *s, const void *qx, const void *qy, int64_t 
   if (p->splits < 0) return set_error("splits must be >= 0"), IDW_E_ARG;
   if (p->ndevices < 0 || p->ndevices > IDW_MAX_DEVICES)
     return set_error("ndevices must be in [0, " + std::to_string(IDW_MAX_DEVICES) + "]"), IDW_E_ARG;
-  if (device_ptrs && p->ndevices > 1)
-    return set_error("a device list needs host buffers (idw_run / idw_run_xy)"), IDW_E_ARG;
   return 0;
 }
 
@@ -257,12 +255,16 @@ int idw_device_count(void) {
 
 const char *idw_last_error(void) { return g_err.c_str(); }
 
+static int run_device_multi(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p,
+                            void *out, cudaStream_t caller, idw_stats *stats);
+
 int idw_run_device(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p, void *out,
                    void *stream, idw_stats *stats) {
   g_err.clear();
   int rc = validate(s, qx, qy, m, p, out, true);
   if (rc) return rc;
   if (m == 0) return 0;
+  if (p->ndevices > 1) return run_device_multi(s, qx, qy, m, p, out, (cudaStream_t)stream, stats);
   cudaStream_t dst;
   int sms;
   const int dev = single_device(p);
@@ -528,6 +530,152 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
   return 0;
 }
 
+// Device-resident form over a device list: the store, queries and output live
+// on devices[0] (the caller's stream belongs to it).  Entry k >= 1 gets the
+// store through the same peer-copy broadcast tree, its query shard by a peer
+// copy from devices[0], runs on its own stream, and its predictions go back
+// into its slice of `out` by a peer copy -- the gather; entry 0 works in
+// place.  Asynchronous: the entries start after the caller's stream reaches
+// the call, and the caller's stream waits for all of them.
+static int run_device_multi(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p,
+                            void *out, cudaStream_t caller, idw_stats *stats) {
+  const int nslot = p->ndevices;
+  const int32_t *devs = p->devices;
+  const size_t esz = s->precision == IDW_SINGLE ? 4 : 8;
+  const int dev0 = devs[0];
+  struct DeviceRestore {
+    int dev = -1;
+    DeviceRestore() {
+      if (cudaGetDevice(&dev) != cudaSuccess) {
+        dev = -1;
+        cudaGetLastError();
+      }
+    }
+    ~DeviceRestore() {
+      if (dev >= 0) cudaSetDevice(dev);
+    }
+  } restore_device;
+  Slot S[IDW_MAX_DEVICES];
+  int uses[64] = {};
+  for (int k = 0; k < nslot; ++k) {
+    if (devs[k] < 0 || devs[k] >= 64) return set_error("device ordinal out of range"), IDW_E_ARG;
+    Slot &sl = S[k];
+    sl.dev = devs[k];
+    if (int rc = slot_stream(sl.dev, uses[sl.dev]++, &sl.st, &sl.sms)) return rc;
+    shard_of(m, nslot, k, &sl.lo, &sl.hi);
+  }
+  if (nslot > 1) enable_peers(devs, nslot);
+  // inputs ready on the caller's stream
+  cudaEvent_t ready = nullptr;
+  IDW_CK(cudaSetDevice(dev0));
+  IDW_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  IDW_CK(cudaEventRecord(ready, caller));
+  cudaEvent_t have[IDW_MAX_DEVICES] = {}, done[IDW_MAX_DEVICES] = {};
+  struct Events {
+    cudaEvent_t *a, *b, r;
+    int n;
+    ~Events() {
+      cudaEventDestroy(r);  // released once their recorded work completes
+      for (int k = 0; k < n; ++k) {
+        if (a[k]) cudaEventDestroy(a[k]);
+        if (b[k]) cudaEventDestroy(b[k]);
+      }
+    }
+  } ev_guard{have, done, ready, nslot};
+  int64_t launches = 0;
+  for (int k = 0; k < nslot; ++k) {
+    Slot &sl = S[k];
+    IDW_CK(cudaSetDevice(sl.dev));
+    IDW_CK(cudaEventCreateWithFlags(&have[k], cudaEventDisableTiming));
+    IDW_CK(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+    IDW_CK(cudaStreamWaitEvent(sl.st, ready, 0));
+  }
+  // A. per entry >= 1: an arena for the store copy, the query shard and the
+  //    output shard; entry 0 reads and writes the caller's buffers in place
+  for (int k = 0; k < nslot; ++k) {
+    Slot &sl = S[k];
+    IDW_CK(cudaSetDevice(sl.dev));
+    const size_t mk = (size_t)(sl.hi - sl.lo);
+    size_t total = 0;
+    auto take = [&](size_t bytes) {
+      size_t o = total;
+      total += (bytes + 255) & ~size_t(255);
+      return o;
+    };
+    for (int b = 0; b < s->nbuf; ++b) sl.off[b] = k ? take((size_t)s->nbytes[b] + 64) : 0;
+    sl.off[3] = k ? take(esz * mk) : 0;
+    sl.off[4] = k ? take(esz * mk) : 0;
+    sl.off[5] = k ? take(esz * mk) : 0;
+    sl.off[6] = take(mk);  // flags
+    IDW_CK(cudaMallocAsync((void **)&sl.arena, total ? total : 256, sl.st));
+  }
+  // B. the store: devices[0] holds it; broadcast tree to the other entries
+  IDW_CK(cudaSetDevice(S[0].dev));
+  IDW_CK(cudaEventRecord(have[0], S[0].st));
+  auto store_ptr = [&](int k, int b) -> unsigned char * {
+    return k ? S[k].arena + S[k].off[b] : (unsigned char *)s->buf[b];
+  };
+  for (int j = 1; j < nslot; ++j) {
+    int top = 1;
+    while (top * 2 <= j) top *= 2;
+    const int src = j - top;
+    Slot &dst = S[j];
+    IDW_CK(cudaSetDevice(dst.dev));
+    IDW_CK(cudaStreamWaitEvent(dst.st, have[src], 0));
+    for (int b = 0; b < s->nbuf; ++b)
+      IDW_CK(cudaMemcpyPeerAsync(store_ptr(j, b), dst.dev, store_ptr(src, b), S[src].dev, (size_t)s->nbytes[b],
+                                 dst.st));
+    IDW_CK(cudaEventRecord(have[j], dst.st));
+  }
+  // C. queries in, kernels, predictions back (the gather), completion
+  for (int k = 0; k < nslot; ++k) {
+    Slot &sl = S[k];
+    const int64_t mk = sl.hi - sl.lo;
+    IDW_CK(cudaSetDevice(sl.dev));
+    if (mk > 0) {
+      const char *qxs = (const char *)qx + esz * sl.lo, *qys = (const char *)qy + esz * sl.lo;
+      char *outs = (char *)out + esz * sl.lo;
+      const void *dq[2] = {qxs, qys};
+      void *dout = outs;
+      if (k) {
+        IDW_CK(cudaMemcpyPeerAsync(sl.arena + sl.off[3], sl.dev, qxs, dev0, esz * (size_t)mk, sl.st));
+        IDW_CK(cudaMemcpyPeerAsync(sl.arena + sl.off[4], sl.dev, qys, dev0, esz * (size_t)mk, sl.st));
+        dq[0] = sl.arena + sl.off[3];
+        dq[1] = sl.arena + sl.off[4];
+        dout = sl.arena + sl.off[5];
+      }
+      const void *dbuf[3] = {nullptr, nullptr, nullptr};
+      for (int b = 0; b < s->nbuf; ++b) dbuf[b] = store_ptr(k, b);
+      Launch &L = sl.L;
+      fill_launch(L, s, dbuf, dq[0], dq[1], mk, p, dout);
+      L.st = sl.st;
+      L.dev = sl.dev;
+      L.sms = sl.sms;
+      if (needs_fixup(L)) L.flags = sl.arena + sl.off[6];
+      if (int rc = dispatch(L)) {
+        cudaFreeAsync(sl.arena, sl.st);
+        for (int j = 0; j < nslot; ++j)
+          if (j != k) {
+            cudaSetDevice(S[j].dev);
+            cudaFreeAsync(S[j].arena, S[j].st);
+          }
+        return rc;
+      }
+      launches += L.launches;
+      if (k) IDW_CK(cudaMemcpyPeerAsync(outs, dev0, sl.arena + sl.off[5], sl.dev, esz * (size_t)mk, sl.st));
+    }
+    IDW_CK(cudaFreeAsync(sl.arena, sl.st));
+    IDW_CK(cudaEventRecord(done[k], sl.st));
+  }
+  IDW_CK(cudaSetDevice(dev0));
+  for (int k = 0; k < nslot; ++k) IDW_CK(cudaStreamWaitEvent(caller, done[k], 0));
+  if (stats) {
+    stats->kernel_launches = launches;
+    stats->merge_events = p->variant == IDW_NESTED_ORIGINAL ? m * ((s->count + p->group_size - 1) / p->group_size) : 0;
+  }
+  return 0;
+}
+
 static void plan_free(idw_plan *pl) {
   if (!pl) return;
   if (pl->exec) cudaGraphExecDestroy(pl->exec);
@@ -546,6 +694,7 @@ int idw_plan_create(const idw_store *s, const void *qx, const void *qy, int64_t 
   int rc = validate(s, qx, qy, m, p, out, true);
   if (rc) return rc;
   if (m == 0) return set_error("a plan needs at least one query"), IDW_E_ARG;
+  if (p->ndevices > 1) return set_error("a plan runs on one device (ndevices <= 1)"), IDW_E_ARG;
   cudaStream_t dst;
   int sms;
   const int dev = single_device(p);

@@ -154,15 +154,20 @@ class DeviceStore:
 def predict_device(dstore: DeviceStore, qx, qy, out, params: Params = Params(),
                    cfg: ExecConfig | None = None, variant: str = "tiled", stream=None):
     """Launch ``variant`` for device tensors qx, qy -> out (run dtype, contiguous)
-    on ``stream`` (default: torch's current stream).  Returns the native stats."""
+    on ``stream`` (default: torch's current stream).  Returns the native stats.
+    ``cfg.devices`` (starting with the store's device) spreads the call over
+    several GPUs: peer-copy broadcast of the store, query shards out and
+    predictions back by peer copies; ``stream`` waits for all of them."""
     import torch
 
     cfg = cfg or ExecConfig()
     m = int(out.shape[0])
     if stream is None:
         stream = torch.cuda.current_stream(dstore.device)
+    if cfg.devices and cfg.devices[0] != dstore.device:
+        raise ValueError(f"device list must start with the store's device {dstore.device}")
     prm = _capi.make_params(params.p, params.zero_eps, variant, cfg.mode, cfg.group_size,
-                            cfg.tile_size, cfg.splits, dstore.device)
+                            cfg.tile_size, cfg.splits, dstore.device, cfg.devices)
     return _capi.run_device(dstore.native(), qx.data_ptr(), qy.data_ptr(), m, prm,
                             out.data_ptr(), stream.cuda_stream)
 

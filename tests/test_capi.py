@@ -73,10 +73,11 @@ def test_device_list_validation():
     ns = _capi.make_store("soa", "double", st.count, [b.ctypes.data for b in st.buffers],
                           [b.nbytes for b in st.buffers])
     q = np.zeros(4)
-    # a device list is a host-buffer feature: device-pointer calls refuse it
-    rc = lib.idw_run_device(ctypes.byref(ns), q.ctypes.data, q.ctypes.data, 4, ctypes.byref(prm),
-                            q.ctypes.data, None, None)
-    assert rc == -1 and b"host buffers" in lib.idw_last_error()
+    # a captured plan runs on one device
+    plan = ctypes.c_void_p()
+    rc = lib.idw_plan_create(ctypes.byref(ns), q.ctypes.data, q.ctypes.data, 4, ctypes.byref(prm),
+                             q.ctypes.data, ctypes.byref(plan))
+    assert rc == -1 and b"one device" in lib.idw_last_error()
     prm.ndevices = 17
     rc = lib.idw_run(ctypes.byref(ns), q.ctypes.data, q.ctypes.data, 4, ctypes.byref(prm), q.ctypes.data, None)
     assert rc == -1 and b"ndevices" in lib.idw_last_error()

@@ -176,3 +176,27 @@ def test_device_list_edges(il):
     bad[299, 1] = np.inf
     with pytest.raises(ValueError, match="invalid coordinate"):
         il.run_tiled(store, bad, il.Params(), il.ExecConfig(mode="fast", devices=(0, 0)))
+
+
+@pytest.mark.parametrize("variant,mode,kind,prec", [
+    ("tiled", "fast", "aoas", "single"), ("tiled", "exact", "soa", "double"),
+    ("nested_improved", "fast", "soa", "single"), ("naive", "fast", "aos", "single")])
+def test_device_resident_device_list(il, variant, mode, kind, prec):
+    """predict_device over a device list (idw_run_device, ABI 2): inputs and
+    output on devices[0], the other entries fed by peer copies and their
+    predictions gathered back by peer copies, asynchronous on the caller's
+    stream -- bitwise equal to one device."""
+    import torch
+
+    from paper_1402_4986_b200.device import DeviceStore, predict_device
+
+    store, queries = cloud(il, 120_000, 3_000, kind, prec)
+    ds = DeviceStore(store, 0)
+    tq = [torch.tensor(queries[:, k].astype(store.precision.dtype), device="cuda") for k in (0, 1)]
+    outs = []
+    for devs in (None, (0, 0), (0, 0, 0, 0, 0)):
+        out = torch.full((len(queries),), float("nan"), dtype=ds.dtype, device="cuda")
+        predict_device(ds, tq[0], tq[1], out, il.Params(), il.ExecConfig(mode=mode, devices=devs), variant)
+        outs.append(out.cpu().numpy())  # ordered after the call on the current stream
+    assert np.array_equal(outs[1], outs[0]) and np.array_equal(outs[2], outs[0])
+    assert not np.any(np.isnan(outs[0]))
