@@ -39,4 +39,11 @@ qs = np.vstack([[[2.0 ** -63.5, 0.0], [0.0, 2.0 ** -63.2]], queries[:100]])
 st = il.build(sub, il.LayoutKind.SoA, il.Precision.single)
 for variant in ("naive", "tiled", "nested_improved"):
     il.STRATEGIES[variant](st, qs, cfg=il.ExecConfig(mode="exact"))
+# device-resident device list (peer-copy broadcast, shards, gather)
+from paper_1402_4986_b200.device import predict_device
+dsb = DeviceStore(big, 0)
+qb = [torch.tensor(a[:4000].astype(np.float32), device="cuda") for a in (qx, qy)]
+ob = torch.empty(4000, dtype=torch.float32, device="cuda")
+predict_device(dsb, qb[0], qb[1], ob, il.Params(), il.ExecConfig(mode="fast", devices=(0, 0, 0)), "tiled")
+torch.cuda.synchronize()
 print("sanitize target done")
