@@ -68,15 +68,16 @@ static Shape shape_grid(long long m, long long slots, int Q, int nc_max) {
 
 // FAST summation chunks: tiles per chunk and chunk count from n alone, so a
 // query's result is the same for every m, shard and device count.  About 128
-// chunks (>= 1 and <= 32 tiles each, <= 2048 chunks): work items small enough
+// chunks (>= 1 and <= 128 tiles each, <= 2048 chunks): work items small enough
 // for the dynamic schedule to end evenly, large enough that a chunk partial
-// costs < 0.1 % of its pairs.  `forced` (ExecConfig.splits) overrides.
+// costs < 0.1 % of its pairs and that the partials of a band (below) stay
+// few.  `forced` (ExecConfig.splits) overrides.
 static void chunk_shape(long long ntiles, int forced, long long *S, long long *tpc) {
   long long t;
   if (forced > 0) {
     t = cdiv(ntiles, std::min<long long>(forced, ntiles));
   } else {
-    t = std::min<long long>(32, std::max<long long>(1, ntiles / 128));
+    t = std::min<long long>(128, std::max<long long>(1, ntiles / 128));
     t = std::max<long long>(t, cdiv(ntiles, 2048));
     // experiment knob (changes the summation order, hence the bits)
     static const long long env_tpc = [] { const char *e = getenv("IDW_TPC"); return e ? atoll(e) : 0ll; }();
@@ -144,9 +145,24 @@ static int launch_tiled_fast_box(Launch &L) {
     threads = (int)w * 32;
     smem_l = (int)w * RING;
   }
-  // ring slots: ~4x the groups a full grid has in flight, so a slot's previous
-  // group is long folded when the slot comes round again
-  const long long R = S > 1 ? std::min<long long>(groups, 4 * cdiv(warps, S) + 4) : 0;
+  // Item order: a store larger than a quarter of L2 is swept by bands of B
+  // groups (chunk-major inside a band), so HBM streams it once per band
+  // instead of once per ~warps/S groups (C5, 10M x 100K: 60.7 GB -> 0.6 GB
+  // read per launch); B holds a band's chunk partials to 64 MB.  The order of
+  // work items never changes the bits (each group folds its chunks in chunk
+  // order).
+  long long B = 1;
+  if (S > 1 && (double)L.n * 4 * sizeof(T) > 32e6) {
+    const long long per_group = S * 2 * QG * (long long)sizeof(T);
+    B = std::max<long long>(1, std::min<long long>(groups, (64ll << 20) / per_group));
+  }
+  static const long long env_band = [] { const char *e = getenv("IDW_BAND"); return e ? atoll(e) : 0ll; }();
+  if (env_band > 0) B = std::min<long long>(groups, env_band);
+  // ring slots: two bands plus ~4x the groups a full grid has in flight, so a
+  // slot's previous group is long folded when the slot comes round again
+  // (R >= B is what progress needs: group g - R then lies in an earlier band,
+  // whose items were all taken before any of g's)
+  const long long R = S > 1 ? std::min<long long>(groups, 2 * B + 4 * cdiv(warps, S) + 4) : 0;
 
   // scratch: [next u64 | pad | done[R] | gen[R] | chunk boxes[S] | partials]
   const size_t ctl = ((size_t)(16 + 8 * R) + 255) / 256 * 256;
@@ -174,6 +190,7 @@ static int launch_tiled_fast_box(Launch &L) {
   cs.S = (int)S;
   cs.tpc = (int)tpc;
   cs.R = (int)R;
+  cs.B = (int)B;
   kern<<<(unsigned)blocks, threads, smem_l, L.st>>>(L.g, L.n, (const T *)L.qx, (const T *)L.qy, L.m,
                                                     make_scal<T>(L), (T *)L.out, L.flags, cs);
   IDW_CK_LAUNCH();

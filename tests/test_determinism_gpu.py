@@ -67,6 +67,27 @@ def test_fast_tiled_c3_full_equals_eight_shards(il):
     assert np.max(np.abs(full[idx] - truth) / np.abs(truth)) <= 1e-5
 
 
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_fast_tiled_banded_order_bits(il, prec):
+    """A store larger than a quarter of L2 (10M points, 160 / 320 MB) is swept
+    in bands of query groups, chunk-major inside a band (idw_tiled.cu): the
+    item order must not change the bits.  One call (band order,
+    several chunks per group in flight) == one call per 256-query shard (a
+    group or two each) == a shard split in 3, and a sample is within the FAST
+    tolerance of the fp64 truth.  fp32: 160 groups in bands of 100, fp64: 320
+    groups in bands of 51 (a short last band in both)."""
+    n, m = 10 * (1 << 20), 160 * 256
+    store, queries = cloud(il, n, m, "aoas", prec)
+    cfg = il.ExecConfig(mode="fast")
+    full = il.run_tiled(store, queries, il.Params(), cfg)
+    one = np.concatenate([il.run_tiled(store, queries[i:i + ALIGN], il.Params(), cfg) for i in range(0, m, ALIGN)])
+    assert np.array_equal(one, full)
+    assert np.array_equal(sharded(il, il.run_tiled, store, queries, 3, il.Params(), cfg), full)
+    idx = np.arange(0, m, m // 16)
+    truth = oracle.truth(store, queries[idx])
+    assert np.max(np.abs(full[idx] - truth) / np.abs(truth)) <= {"single": 1e-5, "double": 1e-12}[prec]
+
+
 @pytest.mark.parametrize("kind,prec,p", [("soa", "single", 2.0), ("aos", "single", 3.5),
                                          ("soa", "double", 2.0), ("hybrid", "double", 3.5),
                                          ("aoas", "single", 1.0)])
