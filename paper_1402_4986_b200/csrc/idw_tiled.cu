@@ -270,3 +270,9 @@ int launch_tiled(Launch &L) {
 }
 
 }  // namespace idw
+
+#ifdef IDW_TRACE
+extern "C" int idw_trace_dump(unsigned long long *host) {
+  return (int)cudaMemcpyFromSymbol(host, idw::g_idw_trace, sizeof(idw::g_idw_trace));
+}
+#endif
