@@ -354,6 +354,10 @@ def run_ours(args):
         mhz = clocks.get("sm_mhz") or 1965.0
         peak = sms * 64 * mhz * 1e6 / dp_ops / 1e9  # nominal 64 DP lanes/clk/SM (62 measured)
         run_clock_peak = peak
+    if variant == "tiled":
+        kname = "k_tiled_chunks" if args.mode == "fast" else "k_tiled"
+    else:  # split-reduce: the warp-team kernel for FAST at 32 <= G <= 1024
+        kname = "k_nested_warps" if args.mode == "fast" else "k_nested"
     roof = {
         "bound": "mufu" if prec == "single" else "fp64",
         "achieved": achieved,
@@ -361,7 +365,7 @@ def run_ours(args):
         "unit": "GPairs/s",
         "frac": achieved / peak,
         "traffic": None,
-        "kernel": ("k_tiled_chunks" if args.mode == "fast" else "k_tiled") if variant == "tiled" else "k_nested",
+        "kernel": kname,
         "kernel_ms": kmain,
         "fixup_ms": kfix,
         "peak_source": "measured: idw_mufu_peak probe (independent rcp.approx chains on all "
@@ -402,14 +406,14 @@ def run_ours(args):
     roof["algorithmic_bytes"] = float(n * srec + 3 * (hi - lo) * e_sz)
     # DRAM traffic of the dominant kernel from the committed ncu --set full
     # capture of the same configuration (profiles/r2, tools/gpu_r2_profiles.sh)
-    caps = {"c1": "prof_c1", "c2": "prof_c2", "c3": "prof_c3", "c5": "prof_c5"}
+    caps = {"c1": "prof_c1", "c2": "prof_c2", "c3": "prof_c3", "c5": "prof_c5"}  # C4's capture is 1M x 16K
     prof = ROOT / "profiles" / "r2" / f"{caps.get(args.config, '-')}.raw.csv"
-    if prof.exists() and args.mode == "fast" and world == 1 and variant == "tiled":
+    if prof.exists() and args.mode == "fast" and world == 1:
         import csv
 
         rows = list(csv.reader(open(prof)))
         kcol = rows[0].index("Kernel Name")
-        row = next((r for r in rows[2:] if "k_tiled_chunks" in r[kcol]), None)
+        row = next((r for r in rows[2:] if r[kcol].split("<")[0].split()[-1] == kname), None)
         d = dict(zip(rows[0], row)) if row else {}
         u = dict(zip(rows[0], rows[1]))
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -419,10 +423,12 @@ def run_ours(args):
             roof["traffic"] = rd + wr
             roof["traffic_read"] = rd
             roof["traffic_write"] = wr
-            roof["traffic_source"] = (f"{prof.relative_to(ROOT)} (ncu --set full, one k_tiled_chunks launch, "
-                                      "same config)")
-            roof["traffic_note"] = ("chunk partials live in an L2-resident ring of group slots (recycled after "
-                                    "each group's fold), so DRAM sees the store, the queries and the outputs")
+            roof["traffic_source"] = f"{prof.relative_to(ROOT)} (ncu --set full, one {kname} launch, same config)"
+            if kname == "k_tiled_chunks":
+                roof["traffic_note"] = (
+                    "chunk partials live in an L2-resident ring of group slots (recycled after each group's fold); "
+                    "a store larger than L2/4 (C5) is swept by bands of query groups, so HBM streams it once per "
+                    "band and the band's partials are written back")
         except (KeyError, ValueError):
             pass
 
