@@ -88,6 +88,38 @@ def test_fast_tiled_banded_order_bits(il, prec):
     assert np.max(np.abs(full[idx] - truth) / np.abs(truth)) <= {"single": 1e-5, "double": 1e-12}[prec]
 
 
+BAND_CHILD = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1402_4986_b200 as il
+x, y, z = il.generate_cloud_arrays({n}, 0)
+qx, qy, _ = il.generate_cloud_arrays({m}, il.query_seed(0))
+st = il.LayoutStore.from_arrays(x, y, z, il.LayoutKind({kind!r}), il.Precision({prec!r}))
+np.save({out!r}, il.run_tiled(st, np.column_stack([qx, qy]), il.Params({p}), il.ExecConfig(mode="fast")))
+"""
+
+
+@pytest.mark.parametrize("kind,prec,p", [("aoas", "single", 2.0), ("soa", "double", 3.5), ("aos", "single", 1.0)])
+def test_fast_tiled_forced_bands_bits(il, tmp_path, kind, prec, p):
+    """Band order forced small (IDW_BAND=3, a child process: the knob is read
+    once per process) at a size where the default is group-major: dozens of
+    bands, a short last band, ring slots reused across bands (groups > R) --
+    bitwise equal to the default order."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    n, m = 300_000, 60_000
+    store, queries = cloud(il, n, m, kind, prec)
+    ref = il.run_tiled(store, queries, il.Params(p), il.ExecConfig(mode="fast"))
+    out = tmp_path / "band.npy"
+    code = BAND_CHILD.format(root=str(Path(__file__).resolve().parents[1]), n=n, m=m, kind=kind, prec=prec, p=p,
+                             out=str(out))
+    subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, IDW_BAND="3"))
+    assert np.array_equal(np.load(out), ref)
+
+
 @pytest.mark.parametrize("kind,prec,p", [("soa", "single", 2.0), ("aos", "single", 3.5),
                                          ("soa", "double", 2.0), ("hybrid", "double", 3.5),
                                          ("aoas", "single", 1.0)])

@@ -10,6 +10,14 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np, torch
 import paper_1402_4986_b200 as il
 from paper_1402_4986_b200.device import DevicePlan, DeviceStore
+if len(sys.argv) > 1 and sys.argv[1] == "band":  # run with IDW_BAND=3: K2 FAST banded order, ring reuse
+    for prec in il.Precision:
+        x, y, z = il.generate_cloud_arrays(60_000, 0)
+        qx, qy, _ = il.generate_cloud_arrays(40_000, 1)
+        st = il.LayoutStore.from_arrays(x, y, z, il.LayoutKind.AoaS, prec)
+        il.run_tiled(st, np.column_stack([qx, qy]), cfg=il.ExecConfig(mode="fast"))
+    torch.cuda.synchronize()
+    sys.exit(0)
 rng = np.random.default_rng(5)
 data = rng.random((3000, 3)); data[:, 2] *= 100
 queries = rng.random((700, 2)); queries[3] = data[9, :2]  # one coincidence -> fix-up
