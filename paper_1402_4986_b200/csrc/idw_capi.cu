@@ -342,8 +342,6 @@ struct Slot {
   size_t off[10] = {};
   cudaEvent_t have_data = nullptr, e0 = nullptr, e1 = nullptr;
   Launch L;
-  unsigned long long nfix = 0;
-  unsigned int bad = 0;
 };
 
 // Host-buffer path shared by idw_run (cast qx/qy given) and idw_run_xy (the
@@ -430,8 +428,8 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
     sl.off[4] = take(esz * mk);
     sl.off[5] = take(esz * mk);
     sl.off[6] = take(mk);
-    sl.off[7] = take(sizeof(unsigned long long));
-    sl.off[8] = take(sizeof(unsigned int));
+    sl.off[7] = take(16);  // fix-up count (u64) and non-finite flag (u32) share one 16-byte word pair
+    sl.off[8] = sl.off[7] + 8;
     sl.off[9] = xy ? take(2 * sizeof(double) * mk) : 0;
     IDW_CK(cudaSetDevice(sl.dev));
     IDW_CK(cudaMallocAsync((void **)&sl.arena, total, sl.st));
@@ -464,7 +462,7 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
     if (mk == 0) continue;
     IDW_CK(cudaSetDevice(sl.dev));
     unsigned char *A = sl.arena;
-    IDW_CK(cudaMemsetAsync(A + sl.off[7], 0, 256 + 256, sl.st));  // nfixed + bad (adjacent 256-B slots)
+    IDW_CK(cudaMemsetAsync(A + sl.off[7], 0, 16, sl.st));  // nfixed + bad
     if (xy) {
       IDW_CK(cudaMemcpyAsync(A + sl.off[9], xy + 2 * sl.lo, 2 * sizeof(double) * (size_t)mk,
                              cudaMemcpyHostToDevice, sl.st));
@@ -492,6 +490,9 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
   }
 
   // D. predictions out, straight into each entry's slice of `out`
+  static thread_local unsigned long long *ctr = nullptr;  // [IDW_MAX_DEVICES][2], pinned, portable
+  if (!ctr) IDW_CK(cudaHostAlloc((void **)&ctr, 2 * sizeof(unsigned long long) * IDW_MAX_DEVICES,
+                                 cudaHostAllocPortable));
   for (int k = 0; k < nslot; ++k) {
     Slot &sl = S[k];
     const int64_t mk = sl.hi - sl.lo;
@@ -499,8 +500,9 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
     IDW_CK(cudaSetDevice(sl.dev));
     IDW_CK(cudaMemcpyAsync((char *)out + esz * sl.lo, sl.arena + sl.off[5], esz * (size_t)mk,
                            cudaMemcpyDeviceToHost, sl.st));
-    IDW_CK(cudaMemcpyAsync(&sl.nfix, sl.arena + sl.off[7], sizeof(sl.nfix), cudaMemcpyDeviceToHost, sl.st));
-    IDW_CK(cudaMemcpyAsync(&sl.bad, sl.arena + sl.off[8], sizeof(sl.bad), cudaMemcpyDeviceToHost, sl.st));
+    // both counters in one copy into pinned memory (truly asynchronous; two
+    // pageable copies cost two blocking round trips per call)
+    IDW_CK(cudaMemcpyAsync(ctr + 2 * k, sl.arena + sl.off[7], 16, cudaMemcpyDeviceToHost, sl.st));
   }
   float kms = 0.f;
   int64_t nfix = 0, launches = 0;
@@ -512,8 +514,8 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
     if (sl.hi == sl.lo) continue;
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, sl.e0, sl.e1) == cudaSuccess) kms = std::max(kms, ms);
-    nfix += (int64_t)sl.nfix;
-    nonfinite |= sl.bad;
+    nfix += (int64_t)ctr[2 * k];
+    nonfinite |= (unsigned int)ctr[2 * k + 1];
     launches += sl.L.launches;
   }
   guard.sync = false;
