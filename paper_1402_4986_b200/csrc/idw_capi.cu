@@ -351,7 +351,7 @@ struct Slot {
 //   B. store: host -> devices[0], then a binomial broadcast tree of
 //      cudaMemcpyPeerAsync (round r: entries [0, 2^r) feed [2^r, 2^(r+1)))
 //   C. per entry: its query shard host -> device, kernels
-//   D. per entry: predictions device -> its slice of the caller's `out`
+//   D. per entry: predictions device -> its slice of the caller's `out` (pinned staging when <= 1 MB)
 // B-C are asynchronous across entries; D comes after every entry's C was
 // issued (a copy into pageable memory returns only when it is done).
 static int run_host(const idw_store *s, const void *qx, const void *qy, const double *xy, int64_t m,
@@ -490,15 +490,20 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
   }
 
   // D. predictions out, straight into each entry's slice of `out`
-  static thread_local unsigned long long *ctr = nullptr;  // [IDW_MAX_DEVICES][2], pinned, portable
-  if (!ctr) IDW_CK(cudaHostAlloc((void **)&ctr, 2 * sizeof(unsigned long long) * IDW_MAX_DEVICES,
+  // A small result (<= 1 MB) is staged through pinned memory: the copies
+  // are then asynchronous (a copy into pageable memory blocks the host per
+  // entry) and one host memcpy moves it into `out`.
+  constexpr size_t STAGE = 1 << 20;
+  static thread_local unsigned long long *ctr = nullptr;  // [IDW_MAX_DEVICES][2] counters + STAGE bytes, pinned
+  if (!ctr) IDW_CK(cudaHostAlloc((void **)&ctr, 2 * sizeof(unsigned long long) * IDW_MAX_DEVICES + STAGE,
                                  cudaHostAllocPortable));
+  char *const stage = (size_t)m * esz <= STAGE ? (char *)(ctr + 2 * IDW_MAX_DEVICES) : nullptr;
   for (int k = 0; k < nslot; ++k) {
     Slot &sl = S[k];
     const int64_t mk = sl.hi - sl.lo;
     if (mk == 0) continue;
     IDW_CK(cudaSetDevice(sl.dev));
-    IDW_CK(cudaMemcpyAsync((char *)out + esz * sl.lo, sl.arena + sl.off[5], esz * (size_t)mk,
+    IDW_CK(cudaMemcpyAsync((stage ? stage : (char *)out) + esz * sl.lo, sl.arena + sl.off[5], esz * (size_t)mk,
                            cudaMemcpyDeviceToHost, sl.st));
     // both counters in one copy into pinned memory (truly asynchronous; two
     // pageable copies cost two blocking round trips per call)
@@ -519,6 +524,7 @@ static int run_host(const idw_store *s, const void *qx, const void *qy, const do
     launches += sl.L.launches;
   }
   guard.sync = false;
+  if (stage) std::memcpy(out, stage, (size_t)m * esz);
   if (stats) {
     stats->kernel_ms = kms;
     stats->fixup_queries = nfix;
