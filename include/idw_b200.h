@@ -158,7 +158,10 @@ int idw_run_xy(const idw_store *store, const double *queries, int64_t m,
  * cudaMemcpyPeerAsync broadcast tree, entry k's query shard by a peer copy,
  * and its predictions come back into its slice of `out` by a peer copy (the
  * gather); `stream` waits for all entries.  Store buffers must stay readable up to
- * nbytes rounded up to 16 bytes (bulk copies move 16-byte granules).  Scratch
+ * nbytes rounded up to 16 bytes (bulk copies move 16-byte granules) and start
+ * on a 16-byte boundary (AoS: 4 / 8 bytes suffice for naive, nested_original
+ * and EXACT nested_improved; tiled and FAST nested_improved stage tiles by
+ * bulk copy) -- IDW_E_ARG otherwise.  Scratch
  * is stream-ordered (cudaMallocAsync).  stats->kernel_ms is not filled here. */
 int idw_run_device(const idw_store *store, const void *qx, const void *qy, int64_t m,
                    const idw_params *prm, void *out, void *stream, idw_stats *stats);

@@ -61,9 +61,10 @@ static int nbuf_of(int kind) {
 
 // device_ptrs: the store buffers are read in place by the kernels, so their
 // alignment matters (host buffers are staged into a 256-byte-aligned arena).
-// K2 stages tiles with cp.async.bulk, which needs a 16-byte-aligned source for
-// every layout; the other variants need 16 bytes where they issue vector
-// loads (every layout but AoS, whose 12/24-byte records take scalar loads).
+// K2 and K3 FAST (k_nested_warps) stage tiles with cp.async.bulk, which needs
+// a 16-byte-aligned source for every layout; the other kernels need 16 bytes
+// where they issue vector loads (every layout but AoS, whose 12/24-byte
+// records take scalar loads).
 static int validate(const idw_store *s, const void *qx, const void *qy, int64_t m, const idw_params *p,
                     const void *out, bool device_ptrs) {
   if (!s || !p) return set_error("null store or params"), IDW_E_ARG;
@@ -78,7 +79,8 @@ static int validate(const idw_store *s, const void *qx, const void *qy, int64_t 
     const int64_t need = s->count * (int64_t)bytes_per_point(s->kind, s->precision, b);
     if (s->nbytes[b] < need) return set_error("store buffer shorter than its shape"), IDW_E_ARG;
     if (device_ptrs && p) {
-      const int align = (s->kind == IDW_AOS && p->variant != IDW_TILED) ? (s->precision == IDW_SINGLE ? 4 : 8) : 16;
+      const bool bulk = p->variant == IDW_TILED || (p->variant == IDW_NESTED_IMPROVED && p->mode == IDW_FAST);
+      const int align = (s->kind == IDW_AOS && !bulk) ? (s->precision == IDW_SINGLE ? 4 : 8) : 16;
       if (((uintptr_t)s->buf[b]) % align != 0)
         return set_error("device store buffer not " + std::to_string(align) + "-byte aligned"), IDW_E_ARG;
     }

@@ -342,6 +342,48 @@ def test_device_resident_path_matches_host_path(il):
     assert 1e12 < rate < 2e13  # ~148 SMs x 16/clk x ~2 GHz
 
 
+@pytest.mark.parametrize("precision", ["single", "double"])
+def test_device_aos_store_alignment(il, precision):
+    """A device AoS store 4 (fp32) / 8 (fp64) bytes off a 16-byte boundary:
+    the kernels that stage tiles with cp.async.bulk (tiled, FAST split-reduce)
+    refuse it with an error instead of a misaligned-address fault (which would
+    poison the CUDA context); the scalar-load kernels run on it and match the
+    host path bitwise; the context stays usable."""
+    import torch
+
+    from paper_1402_4986_b200 import _capi
+
+    rng = np.random.default_rng(61)
+    data = random_records(rng, 5000)
+    queries = random_queries(rng, 700)
+    prec = il.Precision(precision)
+    store = il.build(data, il.LayoutKind.AoS, prec)
+    raw = np.ascontiguousarray(store.buffers[0]).view(np.uint8)
+    e = prec.dtype.itemsize
+    dev = torch.zeros(raw.nbytes + 64, dtype=torch.uint8, device="cuda")
+    dev[e:e + raw.nbytes] = torch.from_numpy(raw).cuda()
+    ptr = dev.data_ptr() + e
+    assert ptr % 16 != 0
+    nstore = _capi.make_store("aos", precision, store.count, [ptr], [raw.nbytes])
+    q = [torch.tensor(queries[:, k].astype(prec.dtype), device="cuda") for k in (0, 1)]
+    out = torch.empty(len(queries), dtype=q[0].dtype, device="cuda")
+    m = len(queries)
+    for variant, mode, ok in (("tiled", "exact", False), ("tiled", "fast", False),
+                              ("nested_improved", "fast", False), ("nested_improved", "exact", True),
+                              ("naive", "fast", True), ("naive", "exact", True)):
+        prm = _capi.make_params(2.0, 0.0, variant, mode, 1024, il.ExecConfig().tile_size)
+        if not ok:
+            with pytest.raises(_capi.NativeError, match="16-byte aligned"):
+                _capi.run_device(nstore, q[0].data_ptr(), q[1].data_ptr(), m, prm, out.data_ptr())
+            continue
+        _capi.run_device(nstore, q[0].data_ptr(), q[1].data_ptr(), m, prm, out.data_ptr())
+        torch.cuda.synchronize()
+        host = il.STRATEGIES[variant](store, queries, cfg=il.ExecConfig(mode=mode))
+        assert np.array_equal(out.cpu().numpy(), host), (variant, mode)
+    torch.cuda.synchronize()  # no sticky error left behind
+    assert np.array_equal(il.run_tiled(store, queries), oracle.predict(store, queries))
+
+
 @pytest.mark.parametrize("scale", [1e-70, 1e-20, 1e-3, 1.0, 1e18, 1e40])
 def test_fast_fp64_general_p_scales(il, scale):
     """FAST fp64 general p (quarter-root series for p in multiples of 1/2,
